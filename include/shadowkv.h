@@ -1,0 +1,144 @@
+/*
+ * shadowkv.h -- C ABI of the B200 (sm_100a) ShadowKV decode-time sparse-attention path.
+ *
+ * ShadowKV (arXiv 2410.21465).  Citations: "P:n" = PAPER.md line n (LaTeX source),
+ * "S:n" = SPEC.md line n, "Rn" = reading n of the register in DESIGN.md.
+ *
+ * Two operations, both asynchronous on the caller's CUDA stream:
+ *   shadowkv_build_cache  -- Algorithm 1 "ShadowKV Pre-filling" minus the SVD
+ *                            (the caller supplies the rank-r factors A, B, R14).
+ *   shadowkv_decode_step  -- Algorithm 2 "ShadowKV Decoding" followed by the sparse
+ *                            attention over outliers + selected chunks + local window
+ *                            ("accurate sparse attention computation with selected KV pairs
+ *                            and static outliers").
+ *
+ * Conventions
+ *   - All pointers are caller-owned; the library never allocates, frees or synchronises.
+ *   - bf16 tensors are passed as uint16_t* holding IEEE bfloat16 bit patterns.
+ *   - "device" pointers are cudaMalloc'd (or torch CUDA) memory on the current device;
+ *     "host-mapped" pointers are page-locked host memory that is mapped into the device
+ *     address space (cudaHostAlloc / cudaHostRegister; under UVA the host pointer itself).
+ *   - All device/host buffers must be 16-byte aligned and densely packed in the stated layout.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Errors: the call validates its arguments on the host before enqueuing anything.  On a
+ *     non-OK status nothing was enqueued and shadowkv_last_error() (thread-local) explains why.
+ *     Faults inside kernels surface at the caller's next synchronisation.
+ *
+ * Symbols: b batch, h_q / h_kv query / KV heads (g = h_q / h_kv, q head hq uses KV head
+ * floor(hq/g), R2), d = head_dim, s = ctx_len, r = rank, c = chunk, o = n_outlier, k = budget,
+ * w = window_ctx; n_c = floor((s - w) / c) chunks on the grid, w_eff = s - n_c*c window tokens
+ * (R8), n_L = n_c - o landmarks per KV head.
+ */
+#ifndef SHADOWKV_H
+#define SHADOWKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SHADOWKV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SKV_API __attribute__((visibility("default")))
+#else
+#define SKV_API
+#endif
+
+typedef enum {
+  SKV_OK = 0,
+  SKV_EINVAL = 1,        /* bad argument (null pointer, size out of range, window overflow) */
+  SKV_EUNSUPPORTED = 2,  /* valid per the paper but not compiled: d != 128, c != 8, g not in {1,2,4,8,16} */
+  SKV_ECUDA = 3,         /* a CUDA runtime call or kernel launch failed */
+  SKV_ESTATE = 4         /* V_host is not page-locked + device-mapped */
+} skv_status;
+
+typedef struct {
+  int32_t batch;        /* b >= 1 requests (uniform ctx_len across the batch)                   */
+  int32_t n_q_heads;    /* h_q                                                                  */
+  int32_t n_kv_heads;   /* h_kv; h_q % h_kv == 0                                                */
+  int32_t head_dim;     /* d; must be 128                                                       */
+  int32_t ctx_len;      /* s; context tokens at absolute positions 0..s-1 (R16)                 */
+  int32_t rank;         /* r; multiple of 16, 16 <= r <= 256 ("SVD rank r")               */
+  int32_t chunk;        /* c; must be 8 ("chunks of eight tokens")                 */
+  int32_t n_outlier;    /* o; 0 <= o < n_c                                              */
+  int32_t budget;       /* k selected chunks per KV head; 1 <= k <= n_L           */
+  int32_t window_ctx;   /* w; context tail kept exact on the GPU (R8)                           */
+  int32_t window_cap;   /* ring capacity in tokens per KV head; >= w_eff + (steps you will run)  */
+} skv_dims;
+
+typedef struct {
+  int32_t rotary_dim;     /* even, 2 <= rotary_dim <= d; dims >= rotary_dim pass through (R15)   */
+  int32_t interleaved;    /* 0: halves layout (x_i, x_{i+rot/2}) [Llama]; 1: pairs (2i, 2i+1) [GLM] */
+  const float *inv_freq;  /* device, rotary_dim/2 fp32; angle = fl32(fl32(t) * inv_freq[i])      */
+} skv_rope;
+
+typedef struct {
+  /* rank-r pre-RoPE key factors: K_pre[b][h][t][:] ~= A[b][t][:] . B[b][h][:][:] */
+  const uint16_t *A;        /* device bf16 [b][s][r]                                           */
+  const uint16_t *B;        /* device bf16 [b][h_kv][r][d]                                     */
+  /* GPU-resident state written by build_cache, read by decode_step */
+  uint16_t *landmarks;      /* device bf16 [b][h_kv][n_c][d]: chunk means of post-RoPE keys on
+                               the full grid; rows of outlier chunks are never scored   */
+  int32_t *outlier_ids;     /* device int32 [b][h_kv][o], ascending                     */
+  uint16_t *K_out;          /* device bf16 [b][h_kv][o*c][d] post-RoPE outlier keys     */
+  uint16_t *V_out;          /* device bf16 [b][h_kv][o*c][d] outlier values                     */
+  uint16_t *K_win;          /* device bf16 [b][h_kv][window_cap][d]: slots [0,w_eff) = context
+                               tail, slot w_eff+step = token generated at decode step `step`    */
+  uint16_t *V_win;          /* device bf16 [b][h_kv][window_cap][d]                             */
+  /* offloaded values V^CPU: all s positions kept; outlier/window rows are never read */
+  const uint16_t *V_host;   /* host-mapped bf16 [b][h_kv][s][d], read zero-copy over PCIe        */
+} skv_layer;
+
+/* Bytes of scratch `workspace` (device, 256-byte aligned) that build_cache and decode_step need
+ * for these dims.  Returns 0 on invalid dims (see shadowkv_last_error). Pure host arithmetic. */
+SKV_API size_t shadowkv_workspace_bytes(const skv_dims *dims);
+
+/* Algorithm 1 for every request and KV head, on `stream`:
+ *   keys    = K_rope if non-NULL (device bf16 [b][h_kv][s][d], post-RoPE),
+ *             else RoPE_t(A[t] . B_h) at absolute positions t (the keys the factors represent);
+ *   C_j     = mean of the c keys of chunk j;   landmarks <- bf16(C)
+ *   m_j     = min_t cos(C_j, k_t) (R10, R11; zero norm -> -1)
+ *   outlier_ids <- the o chunks with smallest m (ties -> lower j, R12), ascending
+ *   K_out, V_out <- keys / values of those chunks; values read zero-copy from V_host
+ *   K_win, V_win slots [0, w_eff) <- the context tail (R8)
+ * Requires V_host page-locked and mapped (checked once here; SKV_ESTATE otherwise). */
+SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
+                                const uint16_t *K_rope, void *workspace, void *stream);
+
+/* One decode step of Algorithm 2 for the whole batch, on `stream`:
+ *   a7  K_win/V_win slot w_eff+step <- k_new, v_new (Alg 2 input K, V; R18)
+ *   a1  l_{hq,j} = <q_hq, L_{h,j}> / sqrt(d) over landmarks j (R6)
+ *   a2  z_{h,j} = max_{hq in group h} (l_{hq,j} - logsumexp_j l_{hq,.})  (= log S2, R4, R5)
+ *   a3  I_h = ArgTopK(z_h, k), ties -> lower chunk id, ascending (R12)
+ *   a4  K~ = RoPE_t(A[t] . B_h) for the k*c tokens of I_h at their absolute positions
+ *   a5  V~ = V_host rows of those tokens, gathered zero-copy over the host link
+ *   a6  out_hq = softmax attention of q_hq over outlier tokens + K~/V~ + window slots
+ *       [0, w_eff+step] (R17)
+ * q      device bf16 [b][h_q][d], post-RoPE at position s+step (R16)
+ * k_new  device bf16 [b][h_kv][d] post-RoPE;  v_new device bf16 [b][h_kv][d]
+ * out    device bf16 [b][h_q][d]
+ * sel_ids   nullable device int32 [b][h_kv][k]  -- parity hook for a3
+ * dbg_keys  nullable device bf16 [b][h_kv][k*c][d] -- parity hook for a4 (rebuilt, post-RoPE)
+ * Requires window_cap >= w_eff + step + 1 (SKV_EINVAL otherwise). */
+SKV_API skv_status shadowkv_decode_step(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
+                                const uint16_t *q, const uint16_t *k_new, const uint16_t *v_new,
+                                int32_t step, uint16_t *out, int32_t *sel_ids, uint16_t *dbg_keys,
+                                void *workspace, void *stream);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+SKV_API const char *shadowkv_last_error(void);
+
+/* SHADOWKV_ABI_VERSION of the loaded library. */
+SKV_API int32_t shadowkv_abi_version(void);
+
+/* Number of kernel launches the last successful decode_step / build_cache enqueued
+ * (evidence for bench.py's gpu_launches count). */
+SKV_API int32_t shadowkv_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHADOWKV_H */

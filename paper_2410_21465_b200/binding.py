@@ -1,0 +1,131 @@
+"""Thin ctypes binding of libshadowkv.so (include/shadowkv.h).  Argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module only turns
+torch tensors into pointers.  There is no CPU fallback: if the library is missing the
+import-time ``load()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libshadowkv.so")
+
+SKV_OK, SKV_EINVAL, SKV_EUNSUPPORTED, SKV_ECUDA, SKV_ESTATE = range(5)
+STATUS_NAMES = {0: "SKV_OK", 1: "SKV_EINVAL", 2: "SKV_EUNSUPPORTED", 3: "SKV_ECUDA", 4: "SKV_ESTATE"}
+EXPORTED = ["shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step",
+            "shadowkv_last_error", "shadowkv_abi_version", "shadowkv_last_launch_count"]
+
+
+class SkvDims(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("batch", "n_q_heads", "n_kv_heads", "head_dim", "ctx_len", "rank", "chunk",
+                 "n_outlier", "budget", "window_ctx", "window_cap")]
+
+
+class SkvRope(ctypes.Structure):
+    _fields_ = [("rotary_dim", ctypes.c_int32), ("interleaved", ctypes.c_int32), ("inv_freq", ctypes.c_void_p)]
+
+
+class SkvLayer(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("A", "B", "landmarks", "outlier_ids", "K_out", "V_out", "K_win", "V_win", "V_host")]
+
+
+class ShadowKVError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the in-tree library (raises if it was not built -- no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    lib.shadowkv_workspace_bytes.restype = ctypes.c_size_t
+    lib.shadowkv_workspace_bytes.argtypes = [P(SkvDims)]
+    lib.shadowkv_build_cache.restype = ctypes.c_int
+    lib.shadowkv_build_cache.argtypes = [P(SkvDims), P(SkvRope), P(SkvLayer), ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p]
+    lib.shadowkv_decode_step.restype = ctypes.c_int
+    lib.shadowkv_decode_step.argtypes = [P(SkvDims), P(SkvRope), P(SkvLayer), ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.shadowkv_last_error.restype = ctypes.c_char_p
+    lib.shadowkv_last_error.argtypes = []
+    lib.shadowkv_abi_version.restype = ctypes.c_int32
+    lib.shadowkv_last_launch_count.restype = ctypes.c_int32
+    _LIB = lib
+    return lib
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _check(st: int):
+    if st != SKV_OK:
+        raise ShadowKVError(st, load().shadowkv_last_error().decode())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def dims_struct(batch, n_q_heads, n_kv_heads, head_dim, ctx_len, rank, chunk, n_outlier, budget,
+                window_ctx, window_cap) -> SkvDims:
+    return SkvDims(batch, n_q_heads, n_kv_heads, head_dim, ctx_len, rank, chunk, n_outlier, budget,
+                   window_ctx, window_cap)
+
+
+def rope_struct(rotary_dim: int, interleaved: bool, inv_freq) -> SkvRope:
+    return SkvRope(rotary_dim, 1 if interleaved else 0, _ptr(inv_freq))
+
+
+def layer_struct(A, B, landmarks, outlier_ids, K_out, V_out, K_win, V_win, V_host) -> SkvLayer:
+    return SkvLayer(_ptr(A), _ptr(B), _ptr(landmarks), _ptr(outlier_ids), _ptr(K_out), _ptr(V_out),
+                    _ptr(K_win), _ptr(V_win), _ptr(V_host))
+
+
+def shadowkv_workspace_bytes(dims: SkvDims) -> int:
+    n = load().shadowkv_workspace_bytes(ctypes.byref(dims))
+    if n == 0:
+        raise ShadowKVError(SKV_EINVAL, load().shadowkv_last_error().decode())
+    return n
+
+
+def shadowkv_build_cache(dims: SkvDims, rope: SkvRope, layer: SkvLayer, K_rope, workspace, stream=None):
+    _check(load().shadowkv_build_cache(ctypes.byref(dims), ctypes.byref(rope), ctypes.byref(layer),
+                                       _ptr(K_rope), _ptr(workspace), _stream_ptr(stream)))
+
+
+def shadowkv_decode_step(dims: SkvDims, rope: SkvRope, layer: SkvLayer, q, k_new, v_new, step: int, out,
+                         sel_ids=None, dbg_keys=None, workspace=None, stream=None):
+    _check(load().shadowkv_decode_step(ctypes.byref(dims), ctypes.byref(rope), ctypes.byref(layer), _ptr(q),
+                                       _ptr(k_new), _ptr(v_new), int(step), _ptr(out), _ptr(sel_ids),
+                                       _ptr(dbg_keys), _ptr(workspace), _stream_ptr(stream)))
+
+
+def shadowkv_last_launch_count() -> int:
+    return int(load().shadowkv_last_launch_count())
+
+
+def shadowkv_abi_version() -> int:
+    return int(load().shadowkv_abi_version())

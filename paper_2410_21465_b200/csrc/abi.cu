@@ -1,0 +1,158 @@
+// C ABI of libshadowkv.so (see include/shadowkv.h): argument validation, workspace carving
+// and kernel orchestration.  Host-side only; kernels live in build.cu / decode.cu.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+
+#include "shadowkv.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+skv_status fail(skv_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Validate dims (S:46, S:189, S:245 error classes) and derive n_c, w_eff (R8).
+skv_status check_dims(const skv_dims* d, skv::Dims* D) {
+  if (!d) return fail(SKV_EINVAL, "dims is NULL");
+  if (d->batch < 1) return fail(SKV_EINVAL, "batch must be >= 1 (got %d)", d->batch);
+  if (d->n_q_heads < 1 || d->n_kv_heads < 1) return fail(SKV_EINVAL, "head counts must be >= 1");
+  if (d->n_q_heads % d->n_kv_heads) return fail(SKV_EINVAL, "n_q_heads %% n_kv_heads != 0 (GQA)");
+  const int g = d->n_q_heads / d->n_kv_heads;
+  if (d->head_dim != 128) return fail(SKV_EUNSUPPORTED, "head_dim must be 128 (got %d)", d->head_dim);
+  if (d->chunk != 8) return fail(SKV_EUNSUPPORTED, "chunk must be 8 (got %d)", d->chunk);
+  if (g != 1 && g != 2 && g != 4 && g != 8 && g != 16)
+    return fail(SKV_EUNSUPPORTED, "GQA group %d not in {1,2,4,8,16}", g);
+  if (d->rank < 16 || d->rank > 256) return fail(SKV_EINVAL, "rank %d out of range [16, 256]", d->rank);
+  if (d->rank % 16) return fail(SKV_EUNSUPPORTED, "rank %d not a multiple of 16", d->rank);
+  if (d->window_ctx < 0) return fail(SKV_EINVAL, "window_ctx must be >= 0");
+  if (d->ctx_len < d->window_ctx + d->chunk)
+    return fail(SKV_EINVAL, "ctx_len %d leaves no chunk outside the window (w=%d, c=%d)", d->ctx_len,
+                d->window_ctx, d->chunk);
+  if (d->ctx_len >= (1 << 24) - 65536) return fail(SKV_EINVAL, "ctx_len must be < 2^24 - 65536 (fp32 positions)");
+  const int n_c = (d->ctx_len - d->window_ctx) / d->chunk;
+  const int w_eff = d->ctx_len - n_c * d->chunk;
+  if (d->n_outlier < 0 || d->n_outlier >= n_c)
+    return fail(SKV_EINVAL, "n_outlier %d must satisfy 0 <= o < n_c = %d", d->n_outlier, n_c);
+  if (d->budget < 1 || d->budget > n_c - d->n_outlier)
+    return fail(SKV_EINVAL, "budget %d must satisfy 1 <= k <= n_L = %d", d->budget, n_c - d->n_outlier);
+  if (d->window_cap < w_eff || d->window_cap < 1)
+    return fail(SKV_EINVAL, "window_cap %d < w_eff %d", d->window_cap, w_eff);
+  *D = skv::Dims{d->batch, d->n_q_heads, d->n_kv_heads, g, d->head_dim, d->ctx_len, d->rank, d->chunk,
+                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff};
+  return SKV_OK;
+}
+
+skv_status check_rope(const skv_rope* r, int head_dim, skv::Rope* R) {
+  if (!r) return fail(SKV_EINVAL, "rope is NULL");
+  if (r->rotary_dim < 2 || r->rotary_dim > head_dim || (r->rotary_dim & 1))
+    return fail(SKV_EINVAL, "rotary_dim %d must be even and in [2, %d]", r->rotary_dim, head_dim);
+  if (!r->inv_freq) return fail(SKV_EINVAL, "rope.inv_freq is NULL");
+  *R = skv::Rope{r->inv_freq, r->rotary_dim, r->interleaved ? 1 : 0};
+  return SKV_OK;
+}
+
+skv_status check_layer(const skv_layer* l, const skv::Dims& D, skv::Layer* Ly) {
+  if (!l) return fail(SKV_EINVAL, "layer is NULL");
+  struct { const void* p; const char* n; bool need; } ptrs[] = {
+      {l->A, "A", true}, {l->B, "B", true}, {l->landmarks, "landmarks", true},
+      {l->outlier_ids, "outlier_ids", D.o > 0}, {l->K_out, "K_out", D.o > 0}, {l->V_out, "V_out", D.o > 0},
+      {l->K_win, "K_win", true}, {l->V_win, "V_win", true}, {l->V_host, "V_host", true}};
+  for (auto& p : ptrs) {
+    if (p.need && !p.p) return fail(SKV_EINVAL, "layer.%s is NULL", p.n);
+    if (p.p && !aligned16(p.p)) return fail(SKV_EINVAL, "layer.%s is not 16-byte aligned", p.n);
+  }
+  *Ly = skv::Layer{l->A, l->B, l->landmarks, l->outlier_ids, l->K_out, l->V_out, l->K_win, l->V_win, l->V_host};
+  return SKV_OK;
+}
+
+size_t ws_bytes(const skv::Dims& D) {
+  size_t a = skv::build_ws_bytes(D, nullptr, nullptr);
+  size_t b = skv::decode_ws_bytes(D, nullptr, nullptr);
+  return a > b ? a : b;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* shadowkv_last_error(void) { return g_err.c_str(); }
+int32_t shadowkv_abi_version(void) { return SHADOWKV_ABI_VERSION; }
+int32_t shadowkv_last_launch_count(void) { return g_launches; }
+
+size_t shadowkv_workspace_bytes(const skv_dims* dims) {
+  skv::Dims D;
+  if (check_dims(dims, &D) != SKV_OK) return 0;
+  return ws_bytes(D);
+}
+
+skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
+                                const uint16_t* K_rope, void* workspace, void* stream) {
+  skv::Dims D; skv::Rope R; skv::Layer Ly;
+  skv_status st;
+  if ((st = check_dims(dims, &D)) != SKV_OK) return st;
+  if ((st = check_rope(rope, D.d, &R)) != SKV_OK) return st;
+  if ((st = check_layer(layer, D, &Ly)) != SKV_OK) return st;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
+  if (K_rope && !aligned16(K_rope)) return fail(SKV_EINVAL, "K_rope is not 16-byte aligned");
+  // V_host must be page-locked and device-mapped at the same address (UVA), P:136 V^CPU
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, Ly.V_host);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(SKV_ECUDA, "cudaPointerGetAttributes(V_host): %s", cudaGetErrorString(e)); }
+  if (attr.type != cudaMemoryTypeHost || attr.devicePointer != (void*)Ly.V_host)
+    return fail(SKV_ESTATE, "V_host must be page-locked host memory mapped at the same device address");
+  skv::BuildWs ws;
+  skv::build_ws_bytes(D, &ws, static_cast<char*>(workspace));
+  int launches = 0;
+  e = skv::launch_build(D, R, Ly, K_rope, ws, static_cast<cudaStream_t>(stream), &launches);
+  if (e != cudaSuccess) return fail(SKV_ECUDA, "build launch failed: %s", cudaGetErrorString(e));
+  g_launches = launches;
+  g_err.clear();
+  return SKV_OK;
+}
+
+skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
+                                const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                                int32_t step, uint16_t* out, int32_t* sel_ids, uint16_t* dbg_keys,
+                                void* workspace, void* stream) {
+  skv::Dims D; skv::Rope R; skv::Layer Ly;
+  skv_status st;
+  if ((st = check_dims(dims, &D)) != SKV_OK) return st;
+  if ((st = check_rope(rope, D.d, &R)) != SKV_OK) return st;
+  if ((st = check_layer(layer, D, &Ly)) != SKV_OK) return st;
+  if (step < 0) return fail(SKV_EINVAL, "step must be >= 0");
+  if (D.w_eff + step + 1 > D.wcap)
+    return fail(SKV_EINVAL, "window overflow: w_eff %d + step %d + 1 > window_cap %d", D.w_eff, step, D.wcap);
+  if (!q || !k_new || !v_new || !out) return fail(SKV_EINVAL, "q, k_new, v_new and out must be non-NULL");
+  if (!aligned16(q) || !aligned16(k_new) || !aligned16(v_new) || !aligned16(out) ||
+      (sel_ids && !aligned16(sel_ids)) || (dbg_keys && !aligned16(dbg_keys)))
+    return fail(SKV_EINVAL, "q/k_new/v_new/out/sel_ids/dbg_keys must be 16-byte aligned");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
+  skv::DecodeWs ws;
+  skv::decode_ws_bytes(D, &ws, static_cast<char*>(workspace));
+  int launches = 0;
+  cudaError_t e = skv::launch_decode(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws,
+                                     static_cast<cudaStream_t>(stream), &launches);
+  if (e != cudaSuccess) return fail(SKV_ECUDA, "decode launch failed: %s", cudaGetErrorString(e));
+  g_launches = launches;
+  g_err.clear();
+  return SKV_OK;
+}
+
+}  // extern "C"

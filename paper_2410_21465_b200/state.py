@@ -1,0 +1,101 @@
+"""Layer-state allocation for the C ABI (plumbing: torch allocates, the library computes).
+
+``Shape`` mirrors skv_dims; ``LayerState`` owns one layer's device tensors (A, B, landmarks,
+outliers, window) plus the pinned, device-mapped host value cache V_host ("Offload the
+rest of values to the CPU").  No arithmetic of the method lives here.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import binding as bd
+
+
+@dataclasses.dataclass(frozen=True)
+class Shape:
+    batch: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ctx_len: int
+    rank: int
+    chunk: int
+    n_outlier: int
+    budget: int
+    window_ctx: int
+    window_cap: int
+
+    @property
+    def n_c(self) -> int:          # grid chunks (window absorbs the ragged tail, DESIGN R8)
+        return (self.ctx_len - self.window_ctx) // self.chunk
+
+    @property
+    def w_eff(self) -> int:
+        return self.ctx_len - self.n_c * self.chunk
+
+    def dims(self) -> bd.SkvDims:
+        return bd.dims_struct(self.batch, self.n_q_heads, self.n_kv_heads, self.head_dim, self.ctx_len,
+                              self.rank, self.chunk, self.n_outlier, self.budget, self.window_ctx,
+                              self.window_cap)
+
+    @classmethod
+    def from_config(cls, cfg, steps: int = 64, batch: int | None = None) -> "Shape":
+        s, w, c = cfg.ctx_len, cfg.window_ctx, cfg.chunk
+        w_eff = s - ((s - w) // c) * c
+        return cls(cfg.batch if batch is None else batch, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, s,
+                   cfg.rank, c, cfg.n_outlier, cfg.budget, w, w_eff + steps)
+
+
+def alloc_workspace(shape: Shape, device="cuda") -> torch.Tensor:
+    n = bd.shadowkv_workspace_bytes(shape.dims())
+    return torch.empty(n + 256, dtype=torch.uint8, device=device)
+
+
+def ws_ptr(ws: torch.Tensor) -> int:
+    p = ws.data_ptr()
+    return (p + 255) & ~255
+
+
+class LayerState:
+    """One layer's tensors for the whole per-GPU batch."""
+
+    def __init__(self, shape: Shape, device="cuda", V_host: torch.Tensor | None = None):
+        self.shape = S = shape
+        b, hk, d = S.batch, S.n_kv_heads, S.head_dim
+        bf = torch.bfloat16
+        self.A = torch.empty(b, S.ctx_len, S.rank, dtype=bf, device=device)
+        self.B = torch.empty(b, hk, S.rank, d, dtype=bf, device=device)
+        self.landmarks = torch.empty(b, hk, S.n_c, d, dtype=bf, device=device)
+        self.outlier_ids = torch.empty(b, hk, max(S.n_outlier, 1), dtype=torch.int32, device=device)
+        oc = max(S.n_outlier * S.chunk, 1)
+        self.K_out = torch.empty(b, hk, oc, d, dtype=bf, device=device)
+        self.V_out = torch.empty(b, hk, oc, d, dtype=bf, device=device)
+        self.K_win = torch.zeros(b, hk, S.window_cap, d, dtype=bf, device=device)
+        self.V_win = torch.zeros(b, hk, S.window_cap, d, dtype=bf, device=device)
+        if V_host is None:
+            V_host = torch.empty(b, hk, S.ctx_len, d, dtype=bf, pin_memory=True)
+        assert V_host.is_pinned() and V_host.shape == (b, hk, S.ctx_len, d)
+        self.V_host = V_host
+
+    def layer(self) -> bd.SkvLayer:
+        return bd.layer_struct(self.A, self.B, self.landmarks, self.outlier_ids, self.K_out, self.V_out,
+                               self.K_win, self.V_win, self.V_host)
+
+    def build(self, rope: bd.SkvRope, workspace: torch.Tensor, K_rope: torch.Tensor | None = None, stream=None):
+        bd.shadowkv_build_cache(self.shape.dims(), rope, self.layer(), K_rope, ws_ptr(workspace), stream)
+
+    def decode(self, rope: bd.SkvRope, q, k_new, v_new, step: int, out, workspace, sel_ids=None,
+               dbg_keys=None, stream=None):
+        bd.shadowkv_decode_step(self.shape.dims(), rope, self.layer(), q, k_new, v_new, step, out, sel_ids,
+                                dbg_keys, ws_ptr(workspace), stream)
+
+
+class RopeTable:
+    """Device copy of the model's fp32 inv_freq table + layout flags (skv_rope)."""
+
+    def __init__(self, inv_freq, rotary_dim: int, interleaved: bool, device="cuda"):
+        self.inv_freq = torch.as_tensor(inv_freq, dtype=torch.float32).to(device).contiguous()
+        self.rotary_dim, self.interleaved = int(rotary_dim), bool(interleaved)
+        self.struct = bd.rope_struct(self.rotary_dim, self.interleaved, self.inv_freq)

@@ -1,0 +1,96 @@
+"""C-ABI checks that need no GPU: the library loads, exports what include/shadowkv.h declares,
+and rejects bad arguments synchronously (SKV_EINVAL / SKV_EUNSUPPORTED) before touching CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import synth
+from paper_2410_21465_b200 import binding as bd
+from paper_2410_21465_b200.state import Shape
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "shadowkv.h")
+
+
+def declared_symbols():
+    src = open(HDR).read()
+    return sorted(set(re.findall(r"\b(shadowkv_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    assert "shadowkv_build_cache" in syms and "shadowkv_decode_step" in syms
+    assert set(syms) == set(bd.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert bd.shadowkv_abi_version() == 1
+
+
+def _dims(**kw):
+    base = dict(batch=1, n_q_heads=32, n_kv_heads=8, head_dim=128, ctx_len=4096, rank=160, chunk=8,
+                n_outlier=4, budget=8, window_ctx=16, window_cap=32)
+    base.update(kw)
+    return bd.SkvDims(**base)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_workspace_bytes_for_every_config(lib, name):
+    shp = Shape.from_config(synth.CONFIGS[name])
+    n = bd.shadowkv_workspace_bytes(shp.dims())
+    assert n > 0 and n % 256 == 0
+
+
+@pytest.mark.parametrize("kw,status,needle", [
+    (dict(budget=507), bd.SKV_EINVAL, "budget"),              # k > n_L
+    (dict(budget=0), bd.SKV_EINVAL, "budget"),
+    (dict(n_outlier=510), bd.SKV_EINVAL, "n_outlier"),        # o >= n_c
+    (dict(rank=8), bd.SKV_EINVAL, "rank"),                    # r out of range
+    (dict(rank=168), bd.SKV_EUNSUPPORTED, "rank"),
+    (dict(head_dim=64), bd.SKV_EUNSUPPORTED, "head_dim"),
+    (dict(chunk=16), bd.SKV_EUNSUPPORTED, "chunk"),
+    (dict(n_q_heads=30), bd.SKV_EINVAL, "GQA"),
+    (dict(n_q_heads=24), bd.SKV_EUNSUPPORTED, "group"),
+    (dict(n_q_heads=96, n_kv_heads=3), bd.SKV_EUNSUPPORTED, "group"),
+    (dict(window_cap=8), bd.SKV_EINVAL, "window_cap"),
+    (dict(ctx_len=20), bd.SKV_EINVAL, "ctx_len"),
+])
+def test_invalid_dims_rejected(lib, kw, status, needle):
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(**kw))) == 0
+    assert needle in lib.shadowkv_last_error().decode()
+    rope = bd.SkvRope(128, 0, 16)
+    layer = bd.SkvLayer(*([16] * 9))
+    st = lib.shadowkv_decode_step(ctypes.byref(_dims(**kw)), ctypes.byref(rope), ctypes.byref(layer),
+                                  16, 16, 16, 0, 16, None, None, 256, None)
+    assert st == status
+
+
+def test_decode_argument_errors_before_any_cuda_call(lib):
+    d = _dims()
+    rope = bd.SkvRope(128, 0, 16)
+    layer = bd.SkvLayer(*([16] * 9))
+    call = lambda **kw: lib.shadowkv_decode_step(
+        ctypes.byref(d), ctypes.byref(kw.get("rope", rope)), ctypes.byref(kw.get("layer", layer)),
+        kw.get("q", 16), 16, 16, kw.get("step", 0), kw.get("out", 16), None, None, kw.get("ws", 256), None)
+    assert call(step=16) == bd.SKV_EINVAL                     # w_eff 16 + 16 + 1 > window_cap 32
+    assert "window overflow" in lib.shadowkv_last_error().decode()
+    assert call(step=-1) == bd.SKV_EINVAL
+    assert call(q=0) == bd.SKV_EINVAL
+    assert call(q=18) == bd.SKV_EINVAL                        # misaligned
+    assert call(ws=0) == bd.SKV_EINVAL
+    assert call(ws=272) == bd.SKV_EINVAL                      # workspace needs 256-B alignment
+    assert call(rope=bd.SkvRope(127, 0, 16)) == bd.SKV_EINVAL  # odd rotary dim
+    assert call(rope=bd.SkvRope(128, 0, 0)) == bd.SKV_EINVAL
+    bad = bd.SkvLayer(*([16] * 8 + [0]))
+    assert call(layer=bad) == bd.SKV_EINVAL and "V_host" in lib.shadowkv_last_error().decode()
+    st = lib.shadowkv_build_cache(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(bad), None, 256, None)
+    assert st == bd.SKV_EINVAL
+    assert lib.shadowkv_decode_step(None, None, None, 0, 0, 0, 0, 0, None, None, 0, None) == bd.SKV_EINVAL
+
+
+def test_python_binding_raises_on_error(lib):
+    with pytest.raises(bd.ShadowKVError, match="SKV_EINVAL"):
+        bd.shadowkv_workspace_bytes(_dims(budget=10_000))

@@ -1,0 +1,134 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on identical seeded inputs.
+
+Tolerances: selection bit-exact except score ties within 1e-5 in z (R1);
+outputs <= 2e-2 max-abs; rebuilt keys <= 1e-2 relative; stored bf16 state <= 1 ulp (R13);
+value copies bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import shadowkv_oracle as O
+from tests.parity import (Problem, assert_bf16_close, check_decode, f64, outliers_valid)
+
+pytestmark = pytest.mark.gpu
+
+C1 = synth.CONFIGS["c1"]
+CASES = {
+    "c1": C1,
+    "glm_g16_interleaved": C1.replace(n_q_heads=32, n_kv_heads=2, rope="glm"),
+    "g1_batch2": C1.replace(batch=2, n_q_heads=8, n_kv_heads=8, ctx_len=2048, budget=4),
+    "g2_rank64": C1.replace(n_q_heads=16, n_kv_heads=8, rank=64, ctx_len=1536),
+    "g8_ragged": C1.replace(n_q_heads=32, n_kv_heads=4, ctx_len=4100, budget=20),
+    "full_budget": C1.replace(ctx_len=1040, n_outlier=3, budget=(1040 - 16) // 8 - 3),
+    "no_outliers": C1.replace(ctx_len=2048, n_outlier=0, budget=16, window_ctx=0),
+    "multi_tile_k": C1.replace(ctx_len=16384, budget=40, n_outlier=9, window_ctx=64),
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU parity tests need a CUDA device (run via gpurun)")
+
+
+def _build_checks(P, ost):
+    c = P.cfg
+    assert_bf16_close(f64(P.st.landmarks), ost.landmarks, what="landmarks")
+    gids = P.st.outlier_ids.cpu().numpy()
+    for bi in range(c.batch):
+        for h in range(c.n_kv_heads):
+            if c.n_outlier == 0:
+                continue
+            assert outliers_valid(gids[bi, h], ost.mincos[bi, h], c.n_outlier), (bi, h, gids[bi, h], ost.outlier_ids[bi, h])
+            if np.array_equal(gids[bi, h], ost.outlier_ids[bi, h]):
+                assert_bf16_close(f64(P.st.K_out[bi, h]), ost.K_out[bi, h], what="K_out")
+                np.testing.assert_array_equal(f64(P.st.V_out[bi, h]), ost.V_out[bi, h])
+    w = P.shape.w_eff
+    assert_bf16_close(f64(P.st.K_win[:, :, :w]), ost.K_win[:, :, :w], what="K_win")
+    np.testing.assert_array_equal(f64(P.st.V_win[:, :, :w]), ost.V_win[:, :, :w])
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_build_parity(name):
+    P = Problem(CASES[name], seed=0)
+    P.gpu_build()
+    _build_checks(P, P.oracle_build())
+
+
+def test_build_parity_given_K_rope():
+    P = Problem(C1.replace(ctx_len=2048), seed=3, K_rope=True)
+    P.gpu_build()
+    _build_checks(P, P.oracle_build())
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("seed", [0, 1])
+def test_decode_parity_identical_state(name, seed):
+    """Oracle-built state bytes fed to both decoders; 3 consecutive steps (window grows)."""
+    P = Problem(CASES[name], seed=seed, steps=4)
+    ost = P.oracle_build()
+    P.load_state_from_oracle(ost)
+    for step in range(3):
+        si = P.step_inputs(step)
+        gout, gsel, gkeys = P.gpu_decode(step, si)
+        oout, osel, oz, okeys, ost = P.oracle_decode(ost, step, si)
+        check_decode(P.cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
+        slot = P.shape.w_eff + step
+        np.testing.assert_array_equal(f64(P.st.K_win[:, :, slot]), f64(si["k_new"]))
+        np.testing.assert_array_equal(f64(P.st.V_win[:, :, slot]), f64(si["v_new"]))
+
+
+@pytest.mark.parametrize("name", ["c1", "glm_g16_interleaved", "g8_ragged"])
+def test_end_to_end_build_then_decode(name):
+    """GPU build -> GPU decode vs oracle build -> oracle decode (states may differ by 1 bf16 ulp)."""
+    P = Problem(CASES[name], seed=5)
+    P.gpu_build()
+    ost = P.oracle_build()
+    c = P.cfg
+    g = c.n_q_heads // c.n_kv_heads
+    overlap, total, exact = 0, 0, 0
+    for step in range(2):
+        si = P.step_inputs(step)
+        gout, gsel, gkeys = P.gpu_decode(step, si)
+        oout, osel, oz, okeys, ost = P.oracle_decode(ost, step, si)
+        for bi in range(c.batch):
+            for h in range(c.n_kv_heads):
+                overlap += len(set(gsel[bi, h]) & set(osel[bi, h])); total += c.budget
+                if np.array_equal(gsel[bi, h], osel[bi, h]):
+                    exact += 1
+                    err = np.abs(gout[bi, h * g:(h + 1) * g] - oout[bi, h * g:(h + 1) * g]).max()
+                    assert err <= 2e-2, err
+    assert overlap >= 0.97 * total and exact >= 1
+
+
+def test_full_size_c2_layer():
+    """BASELINE configs[1] at full size (128K, 48 outliers, k = 256), the bench's launch configuration:
+    GPU build vs oracle build, then decode on identical state bytes."""
+    cfg = synth.CONFIGS["c2"]
+    P = Problem(cfg, seed=1234, steps=2)
+    P.gpu_build()
+    ost = P.oracle_build()
+    _build_checks(P, ost)
+    P.load_state_from_oracle(ost)
+    si = P.step_inputs(0)
+    gout, gsel, gkeys = P.gpu_decode(0, si)
+    oout, osel, oz, okeys, _ = P.oracle_decode(ost, 0, si)
+    check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
+
+
+def test_decode_deterministic_and_unpinned_rejected():
+    from paper_2410_21465_b200 import LayerState, binding as bd
+    P = Problem(C1, seed=2)
+    P.gpu_build()
+    si = P.step_inputs(0)
+    a = P.gpu_decode(0, si)
+    b = P.gpu_decode(0, si)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    bad = LayerState(P.shape, V_host=torch.empty(P.shape.batch, C1.n_kv_heads, C1.ctx_len, 128,
+                                                 dtype=torch.bfloat16).pin_memory())
+    bad.V_host = torch.empty(P.shape.batch, C1.n_kv_heads, C1.ctx_len, 128, dtype=torch.bfloat16)  # pageable
+    with pytest.raises(bd.ShadowKVError, match="SKV_ESTATE"):
+        bad.build(P.rope.struct, P.ws)
