@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""ShadowKV decode-time sparse attention on B200: decode tokens/s at 128K (BASELINE.json configs[1]).
+
+One "step" = one decode step of the whole hot path (score, select, key
+rebuild + RoPE, host value gather, sparse attention) for every layer of the model, i.e. 32
+calls of shadowkv_decode_step over 32 distinct layer states (Llama-3.1-8B shape, batch 1, 128K
+context, rank 160, chunk 8, 48 outliers, k = 256 = 1.56 %).  tokens/s = batch * n_gpus /
+step_time (attention path only; QKV/MLP/weights are outside the path -- DESIGN.md §Measurement).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Multi-GPU (torchrun, one process per GPU): every rank runs its own requests (weak scaling, no
+data-path collective); NCCL is used only for the start barrier and the max-over-ranks time.
+--impl reference times the CPU oracle (oracle/, fp64 numpy) on a bounded sample of the same
+workload (one layer of one request per step), extrapolated to the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decode tokens/s at 128K ctx, 1.56% budget, 1/2/4/8 B200; % of HBM/host roofline"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--breakdown", action="store_true", help="extra untimed pass timing every kernel")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(cfg: synth.Config, n_gpus: int) -> dict:
+    return {"workload": f"{cfg.name}: Llama-3.1-8B-shape decode attention, {cfg.n_layers} layers, batch "
+                        f"{cfg.batch}/GPU, {cfg.ctx_len} ctx, rank {cfg.rank}, chunk {cfg.chunk}, "
+                        f"{cfg.n_outlier} outlier chunks, k={cfg.budget} chunks (1.56%), window {cfg.window_ctx}",
+            "n_q_heads": cfg.n_q_heads, "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
+            "ctx_len": cfg.ctx_len, "layers": cfg.n_layers, "batch_per_gpu": cfg.batch,
+            "global_batch": cfg.batch * n_gpus, "parallelism": f"requests sharded over {n_gpus} GPU(s), no collective",
+            "l2": "inputs > L2: 32 distinct layer states cycled every step (~2.5 GB HBM + 8.6 GB pinned host per GPU)",
+            "values": "offloaded to pinned host DRAM, gathered zero-copy over PCIe each step"}
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks (NVML) sampled during the timed region
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clocks_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "no samples")}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------
+def pinned_pool(nbytes: int) -> torch.Tensor:
+    """One page-locked, device-mapped host buffer (cudaHostRegister portable|mapped)."""
+    buf = torch.empty(nbytes // 2, dtype=torch.bfloat16)
+    err = torch.cuda.cudart().cudaHostRegister(buf.data_ptr(), buf.numel() * 2, 3)
+    if int(err) != 0:
+        raise RuntimeError(f"cudaHostRegister failed: {err}")
+    return buf
+
+
+def measure_dma_h2d(pool: torch.Tensor) -> float:
+    """Pinned host->device copy-engine bandwidth, 1 GiB, best of 5 (GB/s)."""
+    n = min(pool.numel(), 1 << 29)
+    src = pool[:n]
+    dst = torch.empty(n, dtype=pool.dtype, device="cuda")
+    best = 1e30
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); dst.copy_(src, non_blocking=True); e1.record(); e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del dst
+    return n * 2 / best / 1e6
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6553.3), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:  # noqa: BLE001
+            return {}
+    return {}
+
+
+def cpu_baseline(cfg: synth.Config, seed: int, budget_s: float = 15.0):
+    """The oracle as it stands, timed on the host cores: decode of ONE layer of ONE request of the
+    workload, repeated for ~budget_s; extrapolated x n_layers x batch to decode tokens/s."""
+    import numpy as np
+    from oracle import shadowkv_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count()
+    one = cfg.replace(batch=1)
+    L = synth.gen_layer(one, seed, layer=0)
+    inv, rot, il = synth.rope_table(one)
+    f = lambda t: t.to(torch.float64).numpy()
+    A, B, V = f(L["A"]), f(L["B"]), f(L["V"])
+    n_c = (one.ctx_len - one.window_ctx) // one.chunk
+    w_eff = one.ctx_len - n_c * one.chunk
+    st = O.build(A, B, V, inv, rot, il, one.chunk, one.n_outlier, one.window_ctx, w_eff + 1024)
+    times, step = [], 0
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s or len(times) < 2:
+        si = synth.gen_step(one, seed, 0, step)
+        t0 = time.perf_counter()
+        O.decode_step(st, A, B, V, f(si["q"]), f(si["k_new"]), f(si["v_new"]), step, one.budget, inv, rot, il,
+                      one.chunk)
+        times.append(time.perf_counter() - t0)
+        step += 1
+        if step >= 1000:
+            break
+    t_layer = float(np.median(times))
+    return {"value": 1.0 / (cfg.n_layers * t_layer), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"fp64 numpy oracle decode_step of 1 layer x 1 request at {one.ctx_len} ctx, {len(times)} steps, "
+                      f"median {t_layer * 1e3:.1f} ms/layer, extrapolated x{cfg.n_layers} layers (state built untimed)",
+            "t_layer_ms": t_layer * 1e3}
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import shadowkv_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count()
+    one = cfg.replace(batch=1)
+    L = synth.gen_layer(one, args.seed, layer=0)
+    inv, rot, il = synth.rope_table(one)
+    f = lambda t: t.to(torch.float64).numpy()
+    A, B, V = f(L["A"]), f(L["B"]), f(L["V"])
+    n_c = (one.ctx_len - one.window_ctx) // one.chunk
+    w_eff = one.ctx_len - n_c * one.chunk
+    st = O.build(A, B, V, inv, rot, il, one.chunk, one.n_outlier, one.window_ctx, w_eff + args.warmup + args.steps + 2)
+    def one_step(i):
+        si = synth.gen_step(one, args.seed, 0, i)
+        return O.decode_step(st, A, B, V, f(si["q"]), f(si["k_new"]), f(si["v_new"]), i, one.budget, inv, rot, il,
+                             one.chunk)
+    for i in range(args.warmup):
+        one_step(i)
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        one_step(i)
+    t_layer = (time.perf_counter() - t0) / args.steps
+    value = 1.0 / (cfg.n_layers * t_layer)          # one request's decode tokens/s on the host cores
+    sample = (f"each step = fp64 numpy oracle decode_step of 1 layer x 1 request of {cfg.name} "
+              f"({one.ctx_len} ctx); tokens/s extrapolated x{cfg.n_layers} layers")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_layer * cfg.n_layers * cfg.batch * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth/)",
+            "config": workload_config(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace, binding as bd
+
+    dev = "cuda"
+    Lm, b = cfg.n_layers, cfg.batch
+    n_total = args.warmup + 2 * args.steps + args.e2e_steps + 48
+    shape = Shape.from_config(cfg, steps=n_total + 1)
+    inv, rot, il = synth.rope_table(cfg)
+    rope = RopeTable(inv, rot, il, device=dev)
+    ws = alloc_workspace(shape, device=dev)
+    seed = args.seed + 7919 * rank
+
+    # --- states: 32 distinct layers, values in one pinned+mapped host pool -------------------
+    per_layer = b * cfg.n_kv_heads * cfg.ctx_len * cfg.head_dim
+    t_setup = time.perf_counter()
+    pool = pinned_pool(per_layer * 2 * Lm)
+    states = []
+    for l in range(Lm):
+        inp = synth.gen_layer(cfg, seed, layer=l, device=dev)
+        vh = pool[l * per_layer:(l + 1) * per_layer].view(b, cfg.n_kv_heads, cfg.ctx_len, cfg.head_dim)
+        st = LayerState(shape, device=dev, V_host=vh)
+        st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); vh.copy_(inp["V"])
+        st.build(rope.struct, ws)
+        states.append(st)
+        del inp
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    # --- per-step inputs (fresh q every step and layer => fresh selections, alpha ~ 0) --------
+    def step_inputs(i, device):
+        qs, ks, vs = [], [], []
+        for l in range(Lm):
+            si = synth.gen_step(cfg, seed, l, i, device=dev)
+            qs.append(si["q"]); ks.append(si["k_new"]); vs.append(si["v_new"])
+        return torch.stack(qs).to(device), torch.stack(ks).to(device), torch.stack(vs).to(device)
+
+    dev_inputs = [step_inputs(i, dev) for i in range(args.warmup + args.steps)]
+    out = torch.empty(Lm, b, cfg.n_q_heads, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(i, q, kn, vn):
+        for l in range(Lm):
+            states[l].decode(rope.struct, q[l], kn[l], vn[l], i, out[l], ws, stream=stream)
+            launches[0] += bd.shadowkv_last_launch_count()
+
+    for i in range(args.warmup):
+        step(i, *dev_inputs[i])
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches[0] = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.warmup, args.warmup + args.steps):
+            step(i, *dev_inputs[i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    gpu_launches = launches[0]
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = b * world / (ms / 1e3)
+
+    # --- dominant-kernel timing: a second timed pass of K steps with CUDA events recorded on the
+    #     launch stream around the fused sparse-attention kernel of every layer (kept out of the
+    #     `value` pass because an event record between kernels disables their PDL overlap)
+    i1 = args.warmup + args.steps
+    bd.shadowkv_profile_begin(Lm * args.steps + 8, 1 << 2)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    p0.record(stream)
+    for i in range(args.steps):
+        step(i1 + i, *dev_inputs[args.warmup + i])
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof = bd.shadowkv_profile_end()
+    prof_pass_ms = p0.elapsed_time(p1) / args.steps
+
+    # --- e2e: host buffers through the public API, H2D inputs + D2H result inside the region --
+    i0 = args.warmup + 2 * args.steps
+    host_inputs = [tuple(t.cpu().pin_memory() for t in step_inputs(i, "cpu")) for i in range(i0, i0 + args.e2e_steps)]
+    q_d = torch.empty_like(dev_inputs[0][0]); k_d = torch.empty_like(dev_inputs[0][1]); v_d = torch.empty_like(dev_inputs[0][2])
+    out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host_inputs[0]) if host_inputs else 0
+    d2h = out_h.numel() * out_h.element_size()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for j, (qh, kh, vh) in enumerate(host_inputs):
+        q_d.copy_(qh, non_blocking=True); k_d.copy_(kh, non_blocking=True); v_d.copy_(vh, non_blocking=True)
+        step(i0 + j, q_d, k_d, v_d)
+        out_h.copy_(out, non_blocking=True)
+        stream.synchronize()                                   # host reads the step's result
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / max(1, args.e2e_steps)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # --- roofline of the dominant kernel (fused rebuild+gather+attention: host-link bound) -----
+    g_ms, g_cnt = prof["sparse_attn"]
+    g_avg_ms = g_ms / max(g_cnt, 1)
+    host_bytes = b * cfg.n_kv_heads * cfg.budget * cfg.chunk * cfg.head_dim * 2          # HOST_alg per launch
+    host_peak = measure_dma_h2d(pool)
+    achieved = host_bytes / (g_avg_ms * 1e-3) / 1e9
+    traffic = load_ncu_traffic().get("sparse_attn_dram_bytes")
+    roofline = {"bound": "host_link", "kernel": "k_sparse_attn", "achieved": achieved, "peak": host_peak,
+                "unit": "GB/s", "frac": achieved / host_peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": host_bytes, "avg_launch_ms": g_avg_ms, "launches": g_cnt,
+                "share_of_step": g_ms / (prof_pass_ms * args.steps), "timing_pass_ms_per_step": prof_pass_ms,
+                "step_frac_of_roofline": (Lm * host_bytes / (host_peak * 1e9)) / (ms * 1e-3),
+                "peak_note": "pinned H2D copy-engine bandwidth measured live in this run (1 GiB, best of 6); "
+                             "zero-copy SM loads saturate ~51 GB/s (profiles/r01_probe_hostlink.txt)"}
+
+    breakdown = None
+    if args.breakdown:
+        bd.shadowkv_profile_begin(Lm * 5 * 20 + 8, 0x1F)
+        for i in range(20):
+            step(i0 + args.e2e_steps + i, *dev_inputs[i % len(dev_inputs)])
+        torch.cuda.synchronize()
+        breakdown = {k: {"avg_us": v[0] / max(v[1], 1) * 1e3, "launches": v[1]} for k, v in bd.shadowkv_profile_end().items()}
+
+    if rank != 0:
+        return
+    hbm_peak, hbm_src = load_peaks()
+    n_c = shape.n_c
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/; random rank-160 factors)",
+            "config": workload_config(cfg, world),
+            "roofline": roofline,
+            "e2e": {"value": b * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+            "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
+            "setup_s": setup_s}
+    if breakdown:
+        line["kernel_breakdown_us"] = breakdown
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, args.seed)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -70,7 +70,9 @@ typedef struct {
 } skv_dims;
 
 typedef struct {
-  int32_t rotary_dim;     /* even, 2 <= rotary_dim <= d; dims >= rotary_dim pass through (R15)   */
+  int32_t rotary_dim;     /* even, 2 <= rotary_dim <= d; dims >= rotary_dim pass through (R15);
+                             halves layout additionally needs rotary_dim/2 % 8 == 0 (else
+                             SKV_EUNSUPPORTED)                                                  */
   int32_t interleaved;    /* 0: halves layout (x_i, x_{i+rot/2}) [Llama]; 1: pairs (2i, 2i+1) [GLM] */
   const float *inv_freq;  /* device, rotary_dim/2 fp32; angle = fl32(fl32(t) * inv_freq[i])      */
 } skv_rope;
@@ -93,7 +95,10 @@ typedef struct {
 } skv_layer;
 
 /* Bytes of scratch `workspace` (device, 256-byte aligned) that build_cache and decode_step need
- * for these dims.  Returns 0 on invalid dims (see shadowkv_last_error). Pure host arithmetic. */
+ * for these dims.  Returns 0 on invalid dims (see shadowkv_last_error). Pure host arithmetic.
+ * The workspace must be ZERO-FILLED once before its first use (it holds per-(request, KV head)
+ * completion counters that every call leaves at zero); one workspace may serve many layers but
+ * only one stream at a time. */
 SKV_API size_t shadowkv_workspace_bytes(const skv_dims *dims);
 
 /* Algorithm 1 for every request and KV head, on `stream`:
@@ -137,6 +142,19 @@ SKV_API int32_t shadowkv_abi_version(void);
 /* Number of kernel launches the last successful decode_step / build_cache enqueued
  * (evidence for bench.py's gpu_launches count). */
 SKV_API int32_t shadowkv_last_launch_count(void);
+
+/* Optional kernel timing for benchmarks (not needed for correctness).  begin() creates
+ * 2*capacity CUDA events; while active, every decode_step records an event pair on its stream
+ * around each kernel whose id bit is set in kernel_mask (ids: 0 score, 1 select,
+ * 2 fused rebuild+gather+attention, 3 reserved, 4 combine).  end() synchronises on the recorded events, writes
+ * the summed milliseconds and launch counts per id into total_ms[5] / counts[5] (nullable) and
+ * destroys the events.  Not thread-safe; one profiling session per process. */
+SKV_API skv_status shadowkv_profile_begin(int32_t capacity, int32_t kernel_mask);
+/* Tuning aid: when dev_buf (device, >= 4*4096*8 uint64) is non-NULL, decode kernels write
+ * %globaltimer stamps [0 score | 1 select | 2 sparse-attn | 3 merge][CTA < 4096][event < 8] into it.
+ * NULL (the default) disables the stamps. */
+SKV_API skv_status shadowkv_trace_buffer(void *dev_buf);
+SKV_API skv_status shadowkv_profile_end(double *total_ms, int32_t *counts);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,9 @@ LIB_PATH = os.path.join(HERE, "lib", "libshadowkv.so")
 SKV_OK, SKV_EINVAL, SKV_EUNSUPPORTED, SKV_ECUDA, SKV_ESTATE = range(5)
 STATUS_NAMES = {0: "SKV_OK", 1: "SKV_EINVAL", 2: "SKV_EUNSUPPORTED", 3: "SKV_ECUDA", 4: "SKV_ESTATE"}
 EXPORTED = ["shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step",
-            "shadowkv_last_error", "shadowkv_abi_version", "shadowkv_last_launch_count"]
+            "shadowkv_last_error", "shadowkv_abi_version", "shadowkv_last_launch_count",
+            "shadowkv_profile_begin", "shadowkv_profile_end", "shadowkv_trace_buffer"]
+KERNEL_NAMES = ["score", "select", "sparse_attn", "reserved", "combine"]
 
 
 class SkvDims(ctypes.Structure):
@@ -66,6 +68,12 @@ def load(path: str = LIB_PATH):
     lib.shadowkv_last_error.argtypes = []
     lib.shadowkv_abi_version.restype = ctypes.c_int32
     lib.shadowkv_last_launch_count.restype = ctypes.c_int32
+    lib.shadowkv_profile_begin.restype = ctypes.c_int
+    lib.shadowkv_profile_begin.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    lib.shadowkv_profile_end.restype = ctypes.c_int
+    lib.shadowkv_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]
+    lib.shadowkv_trace_buffer.restype = ctypes.c_int
+    lib.shadowkv_trace_buffer.argtypes = [ctypes.c_void_p]
     _LIB = lib
     return lib
 
@@ -129,3 +137,20 @@ def shadowkv_last_launch_count() -> int:
 
 def shadowkv_abi_version() -> int:
     return int(load().shadowkv_abi_version())
+
+
+def shadowkv_profile_begin(capacity: int, kernel_mask: int):
+    _check(load().shadowkv_profile_begin(int(capacity), int(kernel_mask)))
+
+
+def shadowkv_profile_end():
+    """-> {kernel_name: (total_ms, count)}"""
+    ms = (ctypes.c_double * 5)()
+    cnt = (ctypes.c_int32 * 5)()
+    _check(load().shadowkv_profile_end(ms, cnt))
+    return {n: (ms[i], cnt[i]) for i, n in enumerate(KERNEL_NAMES)}
+
+
+def shadowkv_trace_buffer(buf):
+    """Enable (device tensor of >= 4*4096*8 int64) or disable (None) the kernels' globaltimer stamps."""
+    _check(load().shadowkv_trace_buffer(_ptr(buf)))

@@ -62,6 +62,8 @@ skv_status check_rope(const skv_rope* r, int head_dim, skv::Rope* R) {
   if (r->rotary_dim < 2 || r->rotary_dim > head_dim || (r->rotary_dim & 1))
     return fail(SKV_EINVAL, "rotary_dim %d must be even and in [2, %d]", r->rotary_dim, head_dim);
   if (!r->inv_freq) return fail(SKV_EINVAL, "rope.inv_freq is NULL");
+  if (!r->interleaved && (r->rotary_dim / 2) % 8)
+    return fail(SKV_EUNSUPPORTED, "halves-layout rotary_dim %d: rotary_dim/2 must be a multiple of 8", r->rotary_dim);
   *R = skv::Rope{r->inv_freq, r->rotary_dim, r->interleaved ? 1 : 0};
   return SKV_OK;
 }
@@ -88,7 +90,83 @@ size_t ws_bytes(const skv::Dims& D) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------
+// Optional CUDA-event timing of individual kernels inside decode_step (bench.py's roofline).
+// Events are created in shadowkv_profile_begin (outside any timed region); decode_step only
+// records them on its own stream.
+namespace skv {
+struct Profiler {
+  int capacity = 0, mask = 0;            // mask: bit i -> time kernel id i
+  int used = 0;
+  cudaEvent_t* ev = nullptr;             // [capacity][2]
+  int* kid = nullptr;
+  int open_slot[kNumKernelIds];
+};
+void profile_mark(Profiler* p, int kernel, bool end, cudaStream_t st) {
+  if (!(p->mask & (1 << kernel))) return;
+  if (!end) {
+    if (p->used >= p->capacity) { p->open_slot[kernel] = -1; return; }
+    int i = p->used++;
+    p->kid[i] = kernel;
+    p->open_slot[kernel] = i;
+    cudaEventRecord(p->ev[2 * i], st);
+  } else if (p->open_slot[kernel] >= 0) {
+    cudaEventRecord(p->ev[2 * p->open_slot[kernel] + 1], st);
+  }
+}
+}  // namespace skv
+
+namespace {
+skv::Profiler* g_prof = nullptr;
+}
+
 extern "C" {
+
+skv_status shadowkv_profile_begin(int32_t capacity, int32_t kernel_mask) {
+  if (g_prof) return fail(SKV_ESTATE, "profiling already active");
+  if (capacity < 1 || kernel_mask <= 0) return fail(SKV_EINVAL, "capacity and kernel_mask must be positive");
+  auto* p = new skv::Profiler();
+  p->capacity = capacity; p->mask = kernel_mask;
+  p->ev = new cudaEvent_t[2 * (size_t)capacity];
+  p->kid = new int[capacity];
+  for (int i = 0; i < 2 * capacity; ++i) {
+    cudaError_t e = cudaEventCreate(&p->ev[i]);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < i; ++j) cudaEventDestroy(p->ev[j]);
+      delete[] p->ev; delete[] p->kid; delete p;
+      return fail(SKV_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
+    }
+  }
+  g_prof = p;
+  return SKV_OK;
+}
+
+skv_status shadowkv_profile_end(double* total_ms, int32_t* counts) {
+  if (!g_prof) return fail(SKV_ESTATE, "profiling not active");
+  skv::Profiler* p = g_prof;
+  g_prof = nullptr;
+  for (int k = 0; k < skv::kNumKernelIds; ++k) { if (total_ms) total_ms[k] = 0.0; if (counts) counts[k] = 0; }
+  skv_status st = SKV_OK;
+  for (int i = 0; i < p->used; ++i) {
+    if (cudaEventSynchronize(p->ev[2 * i + 1]) != cudaSuccess) { st = fail(SKV_ECUDA, "event sync failed"); break; }
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p->ev[2 * i], p->ev[2 * i + 1]) == cudaSuccess) {
+      if (total_ms) total_ms[p->kid[i]] += ms;
+      if (counts) counts[p->kid[i]] += 1;
+    }
+  }
+  for (int i = 0; i < 2 * p->capacity; ++i) cudaEventDestroy(p->ev[i]);
+  delete[] p->ev; delete[] p->kid; delete p;
+  return st;
+}
+
+
+skv_status shadowkv_trace_buffer(void* dev_buf) {
+  cudaError_t e = skv::set_trace_buffer(dev_buf);
+  if (e == cudaSuccess) e = skv::set_trace_buffer_tc(dev_buf);
+  if (e != cudaSuccess) return fail(SKV_ECUDA, "trace buffer: %s", cudaGetErrorString(e));
+  return SKV_OK;
+}
 
 const char* shadowkv_last_error(void) { return g_err.c_str(); }
 int32_t shadowkv_abi_version(void) { return SHADOWKV_ABI_VERSION; }
@@ -148,7 +226,7 @@ skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, cons
   skv::decode_ws_bytes(D, &ws, static_cast<char*>(workspace));
   int launches = 0;
   cudaError_t e = skv::launch_decode(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws,
-                                     static_cast<cudaStream_t>(stream), &launches);
+                                     static_cast<cudaStream_t>(stream), &launches, g_prof);
   if (e != cudaSuccess) return fail(SKV_ECUDA, "decode launch failed: %s", cudaGetErrorString(e));
   g_launches = launches;
   g_err.clear();

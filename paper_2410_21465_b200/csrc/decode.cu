@@ -1,43 +1,66 @@
-// Algorithm 2 "ShadowKV Decoding" + sparse attention, sm_100a (v1 kernels).
+// Algorithm 2 "ShadowKV Decoding" + sparse attention on sm_100a (v2 pipeline).
 //
-//   k_score<G>          a7 window append; a1 landmark logits l = <q, L_j>/sqrt(d) streamed from
-//                       HBM (16 B/lane, half-warp per landmark row, butterfly reduce), per-block
-//                       softmax partials (max, sum exp) over landmarks only (R3)
-//   k_select<G>         a2 lse + z_j = max_group(l - lse); a3 exact top-k
-//   k_rebuild_gather    a4 K~ = RoPE(A[sel] . B_h) on rebuild blocks, while gather
-//                       blocks pull the selected 2 KB value chunks zero-copy over PCIe;
-//                       the two roles share one launch so the key rebuild hides under the fetch
-//                       (the paper's multi-stream overlap, P:40 / P:460, done inside one grid)
-//   k_attn<G>           a6 split-KV attention over [outliers; K~/V~; window]
-//   k_combine           merge of the split partials (log-sum-exp), bf16 output
+//   k_score<G>        a7 window append; a1 logits l = <q, L_j>/sqrt(d).  Persistent CTAs stream
+//                     128-landmark tiles (32 KB, contiguous) HBM -> smem with cp.async.bulk through
+//                     a 4-stage mbarrier ring; half-warp per landmark row, transpose-reduce over the
+//                     16 lanes; per-tile softmax partials (max, sum exp) over landmarks only (R3).
+//   k_select<G>       a2 lse + z_j = max_group(l - lse) (R4, R5); a3 exact top-k:
+//                     z in smem, one bucket-histogram pass relative to z_max, exact resolution of the
+//                     threshold bucket (ties -> lower j, R12), ascending emit via block scan.
+//   k_sparse_attn<G>  a4+a5+a6 fused per unit of 8 chunks (64 tokens): the CTA first issues the
+//                     selected chunks' values host->smem with cp.async.bulk over PCIe, then
+//                     gathers the factor rows A[t], rebuilds K~ = A.B_h in fp32 registers,
+//                     applies RoPE with lane shuffles, computes q.K~ logits, and once the
+//                     values land does softmax + PV; outlier / window units read K,V from HBM.
+//                     The host fetch of every unit is in flight from the kernel's first
+//                     microseconds, so the key rebuild and attention math hide under it (the
+//                     paper's multi-stream overlap of P:40 / P:460, inside one grid).
+//                     The last unit of each (b, h) to finish (workspace counter) merges the
+//                     per-unit partials with a log-sum-exp combine and writes the bf16 output.
+// Kernels after the first are launched with programmatic dependent launch (PDL).
+#include <cstdlib>
+
 #include "kernels.h"
-#include "keytile.cuh"
 #include "topk.cuh"
 
 namespace skv {
 
+constexpr int kMergeMaxPerLane = 16;   // merge handles n_split <= 512 partial units per (b, h)
+constexpr int kMergeHeads = 4;         // heads whose partial loads are in flight together
+
+
+// optional per-CTA timeline (globaltimer ns) for tuning: [kernel][block < 4096][event < 8]
+__device__ uint64_t* g_trace = nullptr;
+// kernels read g_trace once (TRACE_INIT) so that disabled tracing costs no dependent loads
+#define TRACE_INIT uint64_t* const trace_buf_ = g_trace
+#define trace(kernel, ev)                                                                            \
+  do {                                                                                               \
+    if (trace_buf_ != nullptr && threadIdx.x == 0)                                                   \
+      trace_buf_[((size_t)(kernel) * 4096 + blockIdx.x) * 8 + (ev)] = globaltimer();                 \
+  } while (0)
+cudaError_t set_trace_buffer(void* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof(void*)); }
+
 // ---------------------------------------------------------------------------------------------
-// half-warp transpose-reduce: 16 lanes each hold 16 partial sums v[0..16); afterwards lane `sub`
-// holds the full 16-lane sum of element `sub`.
+// transpose-reduce over the 16 lanes of a half-warp: each lane holds N partial sums (N % 16 == 0);
+// afterwards lane `sub` holds the full sums of elements [sub*N/16, (sub+1)*N/16) in v[0..N/16).
 // ---------------------------------------------------------------------------------------------
-template <int N>
-__device__ __forceinline__ void bstage(float* v, int sub) {
+template <int N, int M>
+__device__ __forceinline__ void rs_stage(float* v, int sub) {
   constexpr int H = N / 2;
-  const bool up = sub & H;
+  const bool up = sub & M;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     float send = up ? v[i] : v[i + H];
     float keep = up ? v[i + H] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, M);
   }
 }
-__device__ __forceinline__ float butterfly16(float* v, int sub) {
-  bstage<16>(v, sub); bstage<8>(v, sub); bstage<4>(v, sub); bstage<2>(v, sub);
-  return v[0];
+template <int N>
+__device__ __forceinline__ void reduce_scatter16(float* v, int sub) {
+  rs_stage<N, 8>(v, sub); rs_stage<N / 2, 4>(v, sub); rs_stage<N / 4, 2>(v, sub); rs_stage<N / 8, 1>(v, sub);
 }
 
-// rows [row0, row0+R) of a 128-dim bf16 matrix (one row per 16 lanes, 8 dims per lane) dotted
-// with G query heads held in registers; returns the dot of row (sub / G) with head (sub % G).
+// R rows (16 B of each per lane) dotted with G q heads; returns dot of row sub/G with head sub%G.
 template <int G>
 __device__ __forceinline__ float rows_dot_q(const uint4* v, const float (&qr)[G][8], int sub) {
   constexpr int R = 16 / G;
@@ -54,7 +77,8 @@ __device__ __forceinline__ float rows_dot_q(const uint4* v, const float (&qr)[G]
       acc[i * G + hq] = a;
     }
   }
-  return butterfly16(acc, sub);
+  reduce_scatter16<16>(acc, sub);
+  return acc[0];
 }
 
 template <int G>
@@ -63,282 +87,684 @@ __device__ __forceinline__ void load_q_regs(const uint16_t* qrow0, int sub, floa
   for (int hq = 0; hq < G; ++hq) unpack8(*reinterpret_cast<const uint4*>(qrow0 + hq * kHeadDim + sub * 8), qr[hq]);
 }
 
-// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool is_outlier(const int32_t* __restrict__ ids, int o, int j) {
+  int lo = 0, hi = o;                       // ids ascending (P:131 output, ABI contract)
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(ids + mid) < j) lo = mid + 1; else hi = mid;
+  }
+  return lo < o && __ldg(ids + lo) == j;
+}
+
+// =============================================================================================
+// a1: landmark scoring
+// =============================================================================================
 template <int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, G >= 16 ? 1 : 2)
 k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids, const uint16_t* __restrict__ q,
-        float* __restrict__ logits, float2* __restrict__ part, int n_sblk, float scale,
+        float* __restrict__ logits, float2* __restrict__ part, int tiles_per_head, float scale,
         const uint16_t* __restrict__ k_new, const uint16_t* __restrict__ v_new, uint16_t* K_win,
         uint16_t* V_win, int step) {
+  TRACE_INIT;
   constexpr int R = 16 / G;
-  __shared__ uint32_t omask[kScoreTile / 32];
-  __shared__ float2 wpart[8][G];
-  const int blk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t* buf = reinterpret_cast<uint16_t*>(smem);                                   // [S][128][128]
+  float* P = reinterpret_cast<float*>(smem + (size_t)kSStages * kSTile * kHeadDim * 2);  // [2][G][128]
+  uint32_t* obits = reinterpret_cast<uint32_t*>(P + 2 * G * kSTile);                   // outlier bitmap of the head
+  __shared__ __align__(8) uint64_t full[kSStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = lane >> 4, sub = lane & 15;
-  const size_t bh = (size_t)b * D.hk + h;
-  const int j0 = blk * kScoreTile;
-  if (tid < kScoreTile / 32) omask[tid] = 0u;
-  if (blk == 0 && tid < 2 * kHeadDim / 8) {           // a7: append the current token (R18)
-    const int arr = tid >> 4, p = tid & 15;
-    const size_t dst = (bh * D.wcap + D.w_eff + step) * kHeadDim + p * 8;
-    const uint16_t* src = (arr ? v_new : k_new) + bh * kHeadDim + p * 8;
+  const int total = D.b * D.hk * tiles_per_head;
+  const int t_begin = (int)((long long)blockIdx.x * total / gridDim.x);
+  const int t_end = (int)((long long)(blockIdx.x + 1) * total / gridDim.x);
+  const int nwords = (D.n_c + 31) >> 5;
+  trace(0, 0);
+  pdl_trigger();                                       // let the select grid become resident early
+  // a7: append the current token's K, V to the window (R18)
+  for (int idx = blockIdx.x * 256 + tid; idx < D.b * D.hk * 32; idx += gridDim.x * 256) {
+    const int bh = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;
+    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + step) * kHeadDim + p * 8;
+    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bh * kHeadDim + p * 8;
     *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
   }
-  __syncthreads();
-  for (int i = tid; i < D.o; i += 256) {
-    int j = oids[bh * D.o + i] - j0;
-    if (j >= 0 && j < kScoreTile) atomicOr(&omask[j >> 5], 1u << (j & 31));
+  if (tid == 0) {
+    for (int st = 0; st < kSStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
   }
+  __syncthreads();
+  auto issue = [&](int it) {                           // thread 0: TMA bulk load of tile t_begin + it
+    const int t = t_begin + it;
+    if (t >= t_end) return;
+    const int bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
+    const int j0 = tile * kSTile, rows = min(kSTile, D.n_c - j0);
+    const int st = it % kSStages;
+    mbar_expect_tx(&full[st], rows * kHeadDim * 2);
+    bulk_g2s(buf + (size_t)st * kSTile * kHeadDim, L + ((size_t)bh * D.n_c + j0) * kHeadDim, rows * kHeadDim * 2, &full[st]);
+  };
+  if (tid == 0)
+    for (int it = 0; it < kSStages - 1; ++it) issue(it);
   float qr[G][8];
-  load_q_regs<G>(q + ((size_t)b * D.hq + (size_t)h * G) * kHeadDim, sub, qr);
-  __syncthreads();
-  const uint16_t* Lbh = L + bh * D.n_c * kHeadDim;
-  float* lg_base = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c;
-  float m_run = -INFINITY, s_run = 0.f;
-  const int my_i = sub / G, my_hq = sub % G;
-#pragma unroll 1
-  for (int rb = 0; rb < kScoreTile / 8; rb += 2 * R) {
-    const int rbase = j0 + warp * (kScoreTile / 8) + rb + half * R;
-    uint4 v[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      int row = rbase + i;
-      v[i] = row < D.n_c ? ld_stream(Lbh + (size_t)row * kHeadDim + sub * 8) : make_uint4(0, 0, 0, 0);
+  int cur_bh = -1;
+  for (int it = 0; t_begin + it < t_end; ++it) {
+    const int t = t_begin + it;
+    if (tid == 0) { fence_proxy_async(); issue(it + kSStages - 1); }
+    const int bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
+    const int b = bh / D.hk, h = bh - b * D.hk;
+    const int j0 = tile * kSTile, rows = min(kSTile, D.n_c - j0);
+    if (bh != cur_bh) {                                // new KV head: q registers + outlier bitmap
+      load_q_regs<G>(q + ((size_t)b * D.hq + (size_t)h * G) * kHeadDim, sub, qr);
+      __syncthreads();
+      for (int w = tid; w < nwords; w += 256) obits[w] = 0u;
+      __syncthreads();
+      for (int i = tid; i < D.o; i += 256) {
+        const int j = oids[(size_t)bh * D.o + i];
+        atomicOr(&obits[j >> 5], 1u << (j & 31));
+      }
+      __syncthreads();
+      cur_bh = bh;
     }
-    const float dot = rows_dot_q<G>(v, qr, sub);
-    const int row = rbase + my_i;
-    if (row < D.n_c) {
-      const int jl = row - j0;
-      const bool is_out = (omask[jl >> 5] >> (jl & 31)) & 1u;
-      const float l = is_out ? -INFINITY : dot * scale;
-      lg_base[(size_t)my_hq * D.n_c + row] = l;
-      if (!is_out) lse_merge(m_run, s_run, l, 1.f);
+    const int st = it % kSStages;
+    float* Pb = P + (it & 1) * G * kSTile;
+    mbar_wait(&full[st], (it / kSStages) & 1);
+    const uint16_t* tb = buf + (size_t)st * kSTile * kHeadDim;
+#pragma unroll
+    for (int rb = 0; rb < 16; rb += 2 * R) {          // warp: rows [16w, 16w+16)
+      const int rl = rb + half * R;
+      uint4 v[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = warp * 16 + rl + i;
+        v[i] = (rl + i < 16 && r < rows) ? reinterpret_cast<const uint4*>(tb + (size_t)r * kHeadDim)[sub]
+                                         : make_uint4(0, 0, 0, 0);
+      }
+      const float dot = rows_dot_q<G>(v, qr, sub);
+      const int il = rl + sub / G, r = warp * 16 + il;
+      if (il < 16 && r < rows) {
+        const int j = j0 + r;
+        Pb[(sub % G) * kSTile + r] = ((obits[j >> 5] >> (j & 31)) & 1u) ? -INFINITY : dot * scale;
+      }
+    }
+    __syncthreads();                                   // Pb complete; stage `st` free for reuse
+    float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c + j0;
+    for (int idx = tid; idx < G * kSTile; idx += 256) {
+      const int hq = idx / kSTile, r = idx - hq * kSTile;
+      if (r < rows) lb[(size_t)hq * D.n_c + r] = Pb[idx];
+    }
+    for (int hq = warp; hq < G; hq += 8) {           // tile softmax partial in slot 4*tile, 3 empty slots
+      float x[kSTile / 32];
+      float m = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < kSTile / 32; ++u) { const int r = lane + 32 * u; x[u] = r < rows ? Pb[hq * kSTile + r] : -INFINITY; m = fmaxf(m, x[u]); }
+      m = warp_max(m);
+      float sm = 0.f;
+      if (m > -INFINITY) {
+#pragma unroll
+        for (int u = 0; u < kSTile / 32; ++u) sm += expf(x[u] - m);
+      }
+      sm = warp_sum(sm);
+      float2* pp = part + ((size_t)b * D.hq + (size_t)h * G + hq) * (tiles_per_head * 4) + tile * 4;
+      if (lane < 4) pp[lane] = lane == 0 ? make_float2(m, sm) : make_float2(-INFINITY, 0.f);
     }
   }
-#pragma unroll
-  for (int msk = G; msk < 32; msk <<= 1) {
-    float m2 = __shfl_xor_sync(0xffffffffu, m_run, msk), s2 = __shfl_xor_sync(0xffffffffu, s_run, msk);
-    lse_merge(m_run, s_run, m2, s2);
-  }
-  if (lane < G) wpart[warp][lane] = make_float2(m_run, s_run);
-  __syncthreads();
-  if (tid < G) {
-    float m = -INFINITY, s = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) lse_merge(m, s, wpart[w][tid].x, wpart[w][tid].y);
-    part[((size_t)b * D.hq + (size_t)h * G + tid) * n_sblk + blk] = make_float2(m, s);
-  }
+  trace(0, 1);
 }
 
-// ---------------------------------------------------------------------------------------------
-template <int G>
-__global__ void __launch_bounds__(1024)
-k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int n_sblk,
-         float* __restrict__ z, int32_t* __restrict__ sel, int32_t* __restrict__ sel_user) {
-  __shared__ TopKSmem<1024> sm;
-  __shared__ float lse[G];
-  const int h = blockIdx.x, b = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t bh = (size_t)b * D.hk + h;
-  if (warp < G) {
-    const float2* p = part + ((size_t)b * D.hq + (size_t)h * G + warp) * n_sblk;
-    float m = -INFINITY, s = 0.f;
-    for (int i = lane; i < n_sblk; i += 32) lse_merge(m, s, p[i].x, p[i].y);
-#pragma unroll
-    for (int msk = 16; msk > 0; msk >>= 1) {
-      float m2 = __shfl_xor_sync(0xffffffffu, m, msk), s2 = __shfl_xor_sync(0xffffffffu, s, msk);
-      lse_merge(m, s, m2, s2);
-    }
-    if (lane == 0) lse[warp] = m + logf(s);
-  }
+// =============================================================================================
+// a2 + a3: normalise, group max, exact top-k
+// =============================================================================================
+__device__ __forceinline__ int zbucket(float z, float zmax) {   // 0 = highest scores; 255 = catch-all
+  return min(255, (int)floorf((zmax - z) * 32.f));
+}
+
+// One cluster of kSelCL CTAs per (request, KV head); CTA `rank` owns landmarks
+// [rank * n_per, (rank + 1) * n_per).  Cluster-wide max / histogram / candidates / prefix are
+// exchanged through distributed shared memory (DSMEM).
+template <int NT>
+__device__ __forceinline__ int block_sum(int x, int* wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  x = __reduce_add_sync(0xffffffffu, x);
+  if (lane == 0) wsum[warp] = x;
   __syncthreads();
-  float* zb = z + bh * D.n_c;
-  const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c;
-  for (int j = tid; j < D.n_c; j += 1024) {
+  int t = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) t += wsum[w];
+  __syncthreads();
+  return t;
+}
+
+template <int G, bool ZSMEM>
+__global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 1)
+k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int n_part,
+         float* __restrict__ zws, int32_t* __restrict__ sel, int32_t* __restrict__ sel_user) {
+  TRACE_INIT;
+  constexpr int NT = kSelThreads, NW = NT / 32;
+  extern __shared__ __align__(16) float zdyn[];
+  __shared__ TopKSmem<NT> tk;
+  __shared__ float lse[G], hm[G], wred[NW][G], wred2[NW][G];
+  __shared__ int hist[256], ghist[256], below[kSelCL], taken_r[kSelCL], info[4];
+  __shared__ int cidx[kSelCandLocal], ccnt;
+  __shared__ uint32_t ckey[kSelCandLocal];
+  __shared__ int aidx[kSelCandLocal], arank[kSelCandLocal];
+  __shared__ uint32_t akey[kSelCandLocal];
+  __shared__ int wtmp[NW * kSelCL], wcnt[NW * 64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t crank = cluster_ctarank();
+  const size_t bh = blockIdx.x / kSelCL;
+  const int b = (int)(bh / D.hk), h = (int)(bh - (size_t)b * D.hk);
+  const int n = D.n_c, k = D.k;
+  const int n_per = (n + kSelCL - 1) / kSelCL;
+  const int lo = min(n, (int)crank * n_per), len = min(n, lo + n_per) - lo;
+  float* z = ZSMEM ? zdyn : zws + bh * n + lo;           // this CTA's z slice
+  const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * n + lo;
+  int32_t* out = sel + bh * k;
+  trace(1, 0);
+  pdl_trigger();                                        // sparse-attn CTAs may start their prologue
+  for (int i = tid; i < 256; i += NT) hist[i] = 0;
+  if (tid < kSelCL) taken_r[tid] = 0;
+  if (tid == 0) { ccnt = 0; info[0] = info[1] = 0; }
+  pdl_wait();
+  trace(1, 1);
+  // ---- lse_hq from the score kernel's partials: NW/G warps per head, fixed-order online merges
+  {
+    const int wph = NW / G > 0 ? NW / G : 1;           // warps per head
+    for (int hq = warp / wph; hq < G; hq += NW / wph) {
+      const int wi = warp % wph;
+      const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + hq) * n_part;
+      float m = -INFINITY, sm = 0.f;
+      for (int i = wi * 32 + lane; i < n_part; i += wph * 32) { const float2 v = ph[i]; lse_merge(m, sm, v.x, v.y); }
+#pragma unroll
+      for (int msk = 16; msk > 0; msk >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, msk), s2 = __shfl_xor_sync(0xffffffffu, sm, msk);
+        lse_merge(m, sm, m2, s2);
+      }
+      if (lane == 0) wred[wi][hq] = m, wred2[wi][hq] = sm;
+    }
+    __syncthreads();
+    if (tid < G) {
+      float m = -INFINITY, sm = 0.f;
+      for (int wi = 0; wi < wph; ++wi) lse_merge(m, sm, wred[wi][tid], wred2[wi][tid]);
+      lse[tid] = m + logf(sm);
+      hm[tid] = m;
+    }
+    __syncthreads();
+  }
+  // max_j z_j = max_g (max_j l_gj - lse_g): known from the partials, no extra pass
+  float zmax = -INFINITY;
+#pragma unroll
+  for (int hq = 0; hq < G; ++hq) zmax = fmaxf(zmax, hm[hq] - lse[hq]);
+  trace(1, 2);
+  // ---- z = max_g (l - lse) on the slice (R4, R5) + bucket histogram
+  for (int j = tid; j < len; j += NT) {
     float zz = -INFINITY;
 #pragma unroll
-    for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lb[(size_t)hq * D.n_c + j] - lse[hq]);
-    zb[j] = zz;
+    for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lb[(size_t)hq * n + j] - lse[hq]);
+    z[j] = zz;
+    if (zz > -INFINITY) atomicAdd(&hist[zbucket(zz, zmax)], 1);
+  }
+  trace(1, 3);
+  cluster_sync_all();                                                   // #1 histograms published
+  trace(1, 4);
+  int hv[kSelCL];                                       // thread i < 256 owns bin i of every rank
+#pragma unroll
+  for (int r = 0; r < kSelCL; ++r) hv[r] = tid < 256 ? ld_dsmem_i32(dsmem_addr(&hist[tid], r)) : 0;
+  if (tid < 256) {
+    int g = 0;
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r) g += hv[r];
+    ghist[tid] = g;
   }
   __syncthreads();
-  int32_t* out = sel + bh * D.k;
-  block_topk_largest<1024>(zb, D.n_c, D.k, out, sm);
-  if (sel_user) {
+  if (warp == 0) {                                      // bucket B holding the k-th largest z
+    int c[8], sacc = 0;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) { c[jj] = ghist[lane * 8 + jj]; sacc += c[jj]; }
+    int pre = sacc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, pre, o); if (lane >= o) pre += y; }
+    pre -= sacc;
+    if (pre < k && k <= pre + sacc) {
+      int cum = pre;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        if (cum + c[jj] >= k) { info[0] = lane * 8 + jj; info[1] = k - cum; break; }
+        cum += c[jj];
+      }
+    }
+  }
+  __syncthreads();
+  const int B = info[0], need = info[1];
+  // per-rank count of elements strictly above the threshold bucket
+#pragma unroll
+  for (int r = 0; r < kSelCL; ++r) {
+    const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
+    if (lane == 0) wtmp[warp * kSelCL + r] = v;
+  }
+  bool fallback = B == 255;
+  if (!fallback) {
+    for (int j = tid; j < len; j += NT) {
+      const float zz = z[j];
+      if (zz > -INFINITY && zbucket(zz, zmax) == B) {
+        const int pos = atomicAdd(&ccnt, 1);
+        if (pos < kSelCandLocal) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < kSelCL) { int t = 0; for (int w = 0; w < NW; ++w) t += wtmp[w * kSelCL + tid]; below[tid] = t; }
+  trace(1, 5);
+  cluster_sync_all();                                                   // #2 candidates published
+  trace(1, 6);
+  int rc[kSelCL], total = 0, cmax = 0;
+#pragma unroll
+  for (int r = 0; r < kSelCL; ++r) rc[r] = fallback ? 0 : ld_dsmem_i32(dsmem_addr(&ccnt, r));
+#pragma unroll
+  for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); }
+  fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal || n_per > 16384;
+  if (!fallback) {
+    // all ranks' candidates -> local smem, then rank: larger z first, ties -> lower index (R12)
+    for (int t = tid; t < total; t += NT) {
+      int r = 0, base = 0;
+#pragma unroll
+      for (int rr = 0; rr < kSelCL; ++rr) { const bool past = t >= base + rc[rr] && rr == r; base += past ? rc[rr] : 0; r += past; }
+      const int c = t - base;
+      aidx[t] = ld_dsmem_i32(dsmem_addr(&cidx[c], r));
+      akey[t] = (uint32_t)ld_dsmem_i32(dsmem_addr(&ckey[c], r));
+      arank[t] = r;
+    }
     __syncthreads();
-    for (int i = tid; i < D.k; i += 1024) sel_user[bh * D.k + i] = out[i];
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTileThreads)
-k_rebuild_gather(Dims D, Rope R, Layer Ly, const int32_t* __restrict__ sel, uint16_t* __restrict__ Kt,
-                 uint16_t* __restrict__ Vt, uint16_t* __restrict__ dbg, int n_gather_blocks) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if ((int)blockIdx.x < n_gather_blocks) {
-    // ---- value gather (a5): 2 KB chunk = 8 tokens x 128 dims, 4 x 16 B per lane, 2 chunks in flight
-    const int total = D.b * D.hk * D.k;
-    const int gw = blockIdx.x * (kTileThreads / 32) + warp, nw = n_gather_blocks * (kTileThreads / 32);
-    for (int c0 = gw * 2; c0 < total; c0 += nw * 2) {
-      uint4 v[2][4];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int ci = c0 + u;
-        if (ci < total) {
-          const int bhi = ci / D.k;
-          const uint16_t* src = Ly.V_host + ((size_t)bhi * D.s + (size_t)sel[ci] * kChunk) * kHeadDim;
-#pragma unroll
-          for (int x = 0; x < 4; ++x) v[u][x] = ld_stream(reinterpret_cast<const uint4*>(src) + lane + 32 * x);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int ci = c0 + u;
-        if (ci < total) {
-          uint4* dst = reinterpret_cast<uint4*>(Vt + (size_t)ci * kChunk * kHeadDim);
-#pragma unroll
-          for (int x = 0; x < 4; ++x) dst[lane + 32 * x] = v[u][x];
-        }
+    for (int t = tid; t < total; t += NT) {
+      const uint32_t u = akey[t];
+      const int j = aidx[t];
+      int rank = 0;
+      for (int c = 0; c < total; ++c) rank += (akey[c] > u) || (akey[c] == u && aidx[c] < j);
+      const bool take = rank < need;
+      if (take) atomicAdd(&taken_r[arank[t]], 1);
+      if (arank[t] == (int)crank) z[j - lo] = take ? INFINITY : -INFINITY;
+    }
+    __syncthreads();
+    int base = 0;
+    for (int r = 0; r < (int)crank; ++r) base += below[r] + taken_r[r];
+    // ---- emit this slice ascending (a3 output)
+    const int rounds = (len + NT - 1) / NT;                           // <= 64 (n_per <= 32768)
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int j = rd * NT + tid;
+      bool f = false;
+      if (j < len) { const float zz = z[j]; f = (zz == INFINITY) || (zz > -INFINITY && zbucket(zz, zmax) < B); }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wcnt[rd * NW + warp] = __popc(bal);
+    }
+    __syncthreads();
+    {
+      int tot;                                           // rounds * NW <= NT (n_per <= 16384)
+      const int mine = tid < rounds * NW ? wcnt[tid] : 0;
+      const int ex = block_exclusive_scan<NT>(mine, tk, &tot);
+      if (tid < rounds * NW) wcnt[tid] = base + ex;
+    }
+    __syncthreads();
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int j = rd * NT + tid;
+      bool f = false;
+      if (j < len) { const float zz = z[j]; f = (zz == INFINITY) || (zz > -INFINITY && zbucket(zz, zmax) < B); }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (f) {
+        const int pos = wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u));
+        out[pos] = lo + j;
+        if (sel_user) sel_user[bh * k + pos] = lo + j;
       }
     }
-    return;
+    cluster_sync_all();                                                 // #3 DSMEM reads finished
+  } else {                   // pathological score distribution: exact radix select on one CTA
+    float* zg = zws + bh * n;
+    if (ZSMEM)
+      for (int j = tid; j < len; j += NT) zg[lo + j] = z[j];
+    __threadfence();
+    cluster_sync_all();
+    if (crank == 0) {
+      block_topk_largest<NT>(zg, n, k, out, tk);
+      __syncthreads();
+      if (sel_user)
+        for (int i = tid; i < k; i += NT) sel_user[bh * k + i] = out[i];
+    }
   }
-  // ---- key rebuild (a4): 16 selected chunks = 128 tokens per block
-  const int rb = blockIdx.x - n_gather_blocks;
-  const int tiles = (D.k + 15) / 16;
-  const int tile = rb % tiles;
-  const size_t bh = rb / tiles;
-  const int b = (int)(bh / D.hk);
-  float* Ks = reinterpret_cast<float*>(smem);
-  size_t ab = (size_t)kTileTok * D.r * 2 + (size_t)D.r * kHeadDim * 2, kt = (size_t)kTileTok * kHeadDim * 4;
-  int* tok = reinterpret_cast<int*>(smem + (ab > kt ? ab : kt));
-  const int ntok = min(kTileTok, (D.k - tile * 16) * kChunk);
-  if (tid < kTileTok) {
-    int ci = tile * 16 + (tid >> 3);
-    tok[tid] = ci < D.k ? sel[bh * D.k + ci] * kChunk + (tid & 7) : 0;
-  }
-  __syncthreads();
-  produce_key_tile(Ly.A + (size_t)b * D.s * D.r, Ly.B + bh * D.r * kHeadDim, nullptr, D.r, tok, ntok,
-                   RopeArgs{R.inv_freq, R.rot, R.interleaved}, smem, Ks);
-  for (int idx = tid; idx < ntok * 16; idx += kTileThreads) {
-    const int il = idx >> 4, p = idx & 15;
-    const float* k = Ks + il * kHeadDim + p * 8;
-    uint4 kb = make_uint4(pack_bf2(k[0], k[1]), pack_bf2(k[2], k[3]), pack_bf2(k[4], k[5]), pack_bf2(k[6], k[7]));
-    const size_t dst = (bh * D.k * kChunk + (size_t)tile * kTileTok + il) * kHeadDim + p * 8;
-    *reinterpret_cast<uint4*>(Kt + dst) = kb;
-    if (dbg) *reinterpret_cast<uint4*>(dbg + dst) = kb;
-  }
+  trace(1, 7);
 }
 
-// ---------------------------------------------------------------------------------------------
+// =============================================================================================
+// a4 + a5 + a6: fused rebuild + host gather + attention over one unit of <= 64 tokens
+// =============================================================================================
+struct AttnSmem {      // byte offsets into dynamic smem
+  int v, a, bmat, q, p, tok, bytes;
+};
+__host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
+  AttnSmem s;
+  int off = 0;
+  s.v = off; off += kUnitTok * kHeadDim * 2;                                 // V tile bf16
+  s.a = off; { int ab = kUnitTok * r * 2; off += ab > kUnitTok * kHeadDim * 2 ? ab : kUnitTok * kHeadDim * 2; }  // A rows | K tile
+  s.bmat = off; off += r * kHeadDim * 2;                                    // B_h
+  s.q = off; off += G * kHeadDim * 4;                                       // q fp32
+  s.p = off; off += G * kUnitTok * 4;                                       // logits / probs
+  s.tok = off; off += kUnitTok * 4;
+  s.bytes = off;
+  return s;
+}
+
 template <int G>
-__global__ void __launch_bounds__(128)
-k_attn(Dims D, Layer Ly, const uint16_t* __restrict__ q, const uint16_t* __restrict__ Kt,
-       const uint16_t* __restrict__ Vt, int step, float* __restrict__ o_part, float2* __restrict__ ml_part,
-       int n_split, float scale) {
-  constexpr int R = 16 / G;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint16_t* Ksm = reinterpret_cast<uint16_t*>(smem);                    // [128][128]
-  uint16_t* Vsm = Ksm + kAttnTile * kHeadDim;                           // [128][128]
-  float* P = reinterpret_cast<float*>(Vsm + kAttnTile * kHeadDim);       // [G][128]
+__global__ void __launch_bounds__(256, 2)
+k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const int32_t* __restrict__ sel, int step,
+              float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
+              int n_split, float scale, uint16_t* __restrict__ dbg, int* __restrict__ counters,
+              uint16_t* __restrict__ out) {
+  TRACE_INIT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const AttnSmem lay = attn_smem_layout(D.r, G);
+  uint16_t* Vs = reinterpret_cast<uint16_t*>(smem + lay.v);
+  uint16_t* As = reinterpret_cast<uint16_t*>(smem + lay.a);     // A rows [64][r]  or K tile [64][128]
+  uint16_t* Bs = reinterpret_cast<uint16_t*>(smem + lay.bmat);  // [r][128]
+  float* qs = reinterpret_cast<float*>(smem + lay.q);           // [G][128]
+  float* P = reinterpret_cast<float*>(smem + lay.p);            // [G][64]
+  int* tok = reinterpret_cast<int*>(smem + lay.tok);
+  __shared__ __align__(8) uint64_t barAB, barV;
   __shared__ float2 ml[G];
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = lane >> 4, sub = lane & 15;
-  const size_t bh = (size_t)b * D.hk + h;
-  const int T_out = D.o * kChunk, T_sel = D.k * kChunk, T_win = D.w_eff + step + 1;
-  const int T = T_out + T_sel + T_win;
-  const int t0 = split * kAttnTile, nt = min(kAttnTile, T - t0);
-  for (int idx = tid; idx < kAttnTile * 16; idx += 128) {
-    const int i = idx >> 4, p = idx & 15, t = t0 + i;
-    uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-    if (i < nt) {
-      size_t off;
-      const uint16_t *Ks, *Vs;
-      if (t < T_out) { off = (bh * T_out + t) * kHeadDim; Ks = Ly.K_out; Vs = Ly.V_out; }
-      else if (t < T_out + T_sel) { off = (bh * T_sel + (t - T_out)) * kHeadDim; Ks = Kt; Vs = Vt; }
-      else { off = (bh * D.wcap + (t - T_out - T_sel)) * kHeadDim; Ks = Ly.K_win; Vs = Ly.V_win; }
-      kv = *reinterpret_cast<const uint4*>(Ks + off + p * 8);
-      vv = *reinterpret_cast<const uint4*>(Vs + off + p * 8);
+  const int BH = D.b * D.hk;
+  const int T_out = D.o * kChunk, T_win = D.w_eff + step + 1;
+  int u = blockIdx.x, kind, bh, ui;
+  if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
+  else {
+    u -= BH * n_sel_u;
+    const int per = n_out_u + n_win_u;
+    bh = u / per; ui = u - bh * per;
+    if (ui < n_out_u) kind = 1; else { kind = 2; ui -= n_out_u; }
+  }
+  const int b = bh / D.hk, h = bh - b * D.hk;
+  const int split = kind == 0 ? ui : (kind == 1 ? n_sel_u + ui : n_sel_u + n_out_u + ui);
+  trace(2, 0);
+  if (tid == 0) { mbar_init(&barAB, 1); mbar_init(&barV, 1); fence_mbar_init(); }
+  // q is a call input: stage it before waiting on the producer kernels
+  for (int i = tid; i < G * kHeadDim; i += 256)
+    qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
+  __syncthreads();
+  int ntok;
+  const int tx = tid & 15, ty = tid >> 4;      // key-tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
+  float acc[4][8];
+  if (kind == 0) {
+    const size_t bbytes = (size_t)D.r * kHeadDim * 2;
+    if (tid == 0) {   // B_h does not depend on the selection: fetch it before the PDL wait
+      asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&barAB)), "r"((uint32_t)bbytes) : "memory");
+      bulk_g2s(Bs, Ly.B + (size_t)bh * D.r * kHeadDim, (uint32_t)bbytes, &barAB);
     }
-    reinterpret_cast<uint4*>(Ksm)[idx] = kv;
-    reinterpret_cast<uint4*>(Vsm)[idx] = vv;
+    pdl_wait();
+    trace(2, 1);
+    const int nch = min(8, D.k - ui * 8);
+    ntok = nch * kChunk;
+    if (tid < kUnitTok) tok[tid] = tid < ntok ? sel[(size_t)bh * D.k + ui * 8 + (tid >> 3)] * kChunk + (tid & 7) : 0;
+    if (tid == 0) {
+      const int32_t* ids = sel + (size_t)bh * D.k + ui * 8;
+      // a4 operands first (HBM, needed first): 8 contiguous factor rows per chunk (2.5 KB at r = 160)
+      const uint32_t rb = kChunk * D.r * 2;
+      mbar_expect_tx(&barAB, nch * rb);
+      for (int c = 0; c < nch; ++c)
+        bulk_g2s(As + c * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)ids[c] * kChunk) * D.r, rb, &barAB);
+      // a5: value chunks straight from pinned host memory over PCIe (zero-copy bulk copies)
+      mbar_expect_tx(&barV, nch * kChunk * kHeadDim * 2);
+      for (int c = 0; c < nch; ++c)
+        bulk_g2s(Vs + c * kChunk * kHeadDim,
+                 Ly.V_host + ((size_t)bh * D.s + (size_t)ids[c] * kChunk) * kHeadDim, kChunk * kHeadDim * 2, &barV);
+    }
+    trace(2, 2);
+    __syncthreads();
+    mbar_wait(&barAB, 0);
+    trace(2, 3);
+    // ---- K~ = A_rows . B_h (fp32)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
+    const int r = D.r;
+    for (int rho = 0; rho < r; rho += 2) {
+      float b0[8], b1[8];
+      unpack8(*reinterpret_cast<const uint4*>(Bs + rho * kHeadDim + tx * 8), b0);
+      unpack8(*reinterpret_cast<const uint4*>(Bs + (rho + 1) * kHeadDim + tx * 8), b1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(As + (ty + 16 * i) * r + rho);
+        const float a0 = bf_lo(a2), a1 = bf_hi(a2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[i][e] = fmaf(a1, b1[e], fmaf(a0, b0[e], acc[i][e]));
+      }
+    }
+    // ---- RoPE at the tokens' absolute positions (R15), in registers
+    const int halfrot = R.rot >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int t = tok[ty + 16 * i];
+      if (R.interleaved) {
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const int d0 = tx * 8 + e;
+          if (d0 < R.rot) {
+            float sn, cs;
+            rope_sincos(t, R.inv_freq[d0 >> 1], &sn, &cs);
+            const float x0 = acc[i][e], x1 = acc[i][e + 1];
+            acc[i][e] = x0 * cs - x1 * sn;
+            acc[i][e + 1] = x1 * cs + x0 * sn;
+          }
+        }
+      } else {
+        const int sh = halfrot >> 3;                       // partner lane offset (halfrot % 8 == 0)
+        const bool lowh = tx * 8 < halfrot, inrot = tx * 8 < R.rot;
+        const int src = (lane & 16) | (lowh ? tx + sh : tx - sh) & 15;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float pv = __shfl_sync(0xffffffffu, acc[i][e], inrot ? src : lane);
+          if (inrot) {
+            const int pi = (lowh ? tx * 8 : tx * 8 - halfrot) + e;
+            float sn, cs;
+            rope_sincos(t, R.inv_freq[pi], &sn, &cs);
+            acc[i][e] = lowh ? acc[i][e] * cs - pv * sn : acc[i][e] * cs + pv * sn;
+          }
+        }
+      }
+    }
+    if (dbg) {                                             // a4 parity hook (bf16 of the fp32 keys)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = ty + 16 * i;
+        if (row < ntok) {
+          uint4 kb = make_uint4(pack_bf2(acc[i][0], acc[i][1]), pack_bf2(acc[i][2], acc[i][3]),
+                                pack_bf2(acc[i][4], acc[i][5]), pack_bf2(acc[i][6], acc[i][7]));
+          *reinterpret_cast<uint4*>(dbg + (((size_t)bh * D.k * kChunk) + ui * kUnitTok + row) * kHeadDim + tx * 8) = kb;
+        }
+      }
+    }
+  } else {
+    // ---- outlier or window (R8, R18) unit: exact keys and values from HBM
+    pdl_wait();
+    const uint16_t *Ksrc, *Vsrc;
+    if (kind == 1) {
+      ntok = min(kUnitTok, T_out - ui * kUnitTok);
+      Ksrc = Ly.K_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
+      Vsrc = Ly.V_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
+    } else {
+      ntok = min(kUnitTok, T_win - ui * kUnitTok);
+      Ksrc = Ly.K_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
+      Vsrc = Ly.V_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
+    }
+    if (tid == 0) {
+      mbar_expect_tx(&barAB, ntok * kHeadDim * 2);
+      bulk_g2s(As, Ksrc, ntok * kHeadDim * 2, &barAB);
+      mbar_expect_tx(&barV, ntok * kHeadDim * 2);
+      bulk_g2s(Vs, Vsrc, ntok * kHeadDim * 2, &barV);
+    }
+    mbar_wait(&barAB, 0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = ty + 16 * i;
+      if (row < ntok) unpack8(*reinterpret_cast<const uint4*>(As + row * kHeadDim + tx * 8), acc[i]);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
+      }
+    }
   }
-  float qr[G][8];
-  load_q_regs<G>(q + ((size_t)b * D.hq + (size_t)h * G) * kHeadDim, sub, qr);
+  // ---- logits q . k for G heads: 4 tokens x (<= 4 heads) per lane per pass, reduced over 16 lanes
+  {
+    constexpr int HC = G < 4 ? G : 4;
+#pragma unroll
+    for (int h0 = 0; h0 < G; h0 += HC) {
+      float pv[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) pv[x] = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < HC; ++hh) {
+        const float4* qp = reinterpret_cast<const float4*>(qs + (h0 + hh) * kHeadDim + tx * 8);
+        const float4 q0 = qp[0], q1 = qp[1];
+        const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float a = 0.f;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) a = fmaf(qv[e], acc[i][e], a);
+          pv[i * HC + hh] = a;
+        }
+      }
+      reduce_scatter16<16>(pv, sub);
+      if (sub < 4 * HC) {
+        const int i = sub / HC, hq = h0 + sub % HC, row = ty + 16 * i;
+        P[hq * kUnitTok + row] = row < ntok ? pv[0] * scale : -INFINITY;
+      }
+    }
+  }
   __syncthreads();
-  // logits: 8 half-warps x 16 rows each
-  const int hw = warp * 2 + half;
-#pragma unroll 1
-  for (int rb = 0; rb < 16; rb += R) {
-    const int r0 = hw * 16 + rb;
-    uint4 v[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = reinterpret_cast<const uint4*>(Ksm + (r0 + i) * kHeadDim)[sub];
-    const float dot = rows_dot_q<G>(v, qr, sub);
-    const int row = r0 + sub / G;
-    P[(sub % G) * kAttnTile + row] = row < nt ? dot * scale : -INFINITY;
+  // ---- softmax statistics of this unit (per q head)
+  for (int hq = warp; hq < G; hq += 8) {
+    float x0 = P[hq * kUnitTok + lane], x1 = P[hq * kUnitTok + lane + 32];
+    const float m = warp_max(fmaxf(x0, x1));
+    const float e0 = expf(x0 - m), e1 = expf(x1 - m);
+    P[hq * kUnitTok + lane] = e0;
+    P[hq * kUnitTok + lane + 32] = e1;
+    const float l = warp_sum(e0 + e1);
+    if (lane == 0) ml[hq] = make_float2(m, l);
   }
+  trace(2, 4);
+  mbar_wait(&barV, 0);                                   // values (from PCIe for selected units)
+  trace(2, 5);
   __syncthreads();
-  // per-head max / exp / sum (warp w handles heads w, w+4, ...)
-  for (int hq = warp; hq < G; hq += 4) {
-    float x[4], m = -INFINITY;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { x[u] = P[hq * kAttnTile + lane + 32 * u]; m = fmaxf(m, x[u]); }
-    m = warp_max(m);
-    float s = 0.f;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { float e = expf(x[u] - m); P[hq * kAttnTile + lane + 32 * u] = e; s += e; }
-    s = warp_sum(s);
-    if (lane == 0) ml[hq] = make_float2(m, s);
-  }
-  __syncthreads();
-  // PV: thread = output dim
-  float acc[G];
-#pragma unroll
-  for (int hq = 0; hq < G; ++hq) acc[hq] = 0.f;
-  for (int t = 0; t < nt; ++t) {
-    const float v = bf2f(Vsm[t * kHeadDim + tid]);
-#pragma unroll
-    for (int hq = 0; hq < G; ++hq) acc[hq] = fmaf(P[hq * kAttnTile + t], v, acc[hq]);
-  }
-#pragma unroll
-  for (int hq = 0; hq < G; ++hq) {
+  // ---- PV: thread = (dim, head parity)
+  const int d = tid & 127, hh = tid >> 7;
+  for (int hq = hh; hq < G; hq += 2) {
+    float a = 0.f;
+    for (int t = 0; t < ntok; ++t) a = fmaf(P[hq * kUnitTok + t], bf2f(Vs[t * kHeadDim + d]), a);
     const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-    o_part[row * kHeadDim + tid] = acc[hq];
-    if (tid == 0) ml_part[row] = ml[hq];
+    o_part[row * kHeadDim + d] = a;
+    if (d == 0) ml_part[row] = ml[hq];
   }
+  // ---- the last unit of this (b, h) to finish merges all partials (log-sum-exp) -> out
+  __shared__ int is_last;
+  __syncthreads();                                     // all partial stores of this CTA issued
+  if (tid == 0) {
+    __threadfence();                                   // cumulative release of the CTA's partials
+    is_last = atomicAdd(&counters[bh], 1) == n_split - 1;
+    if (is_last) __threadfence();                      // acquire the other units' partials
+  }
+  trace(2, 6);
+  __syncthreads();
+  if (!is_last) return;
+  float* wsm = reinterpret_cast<float*>(smem + lay.a);          // [G][n_split] weights (A/B region is free)
+  trace(3, 0);
+  for (int hq = warp; hq < G; hq += 8) {
+    const float2* mlr = ml_part + ((size_t)b * D.hq + (size_t)h * G + hq) * n_split;
+    float2 v[kMergeMaxPerLane];
+#pragma unroll
+    for (int u = 0; u < kMergeMaxPerLane; ++u) {
+      const int s2 = lane + 32 * u;
+      v[u] = s2 < n_split ? __ldcg(&mlr[s2]) : make_float2(-INFINITY, 0.f);
+    }
+    float M = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < kMergeMaxPerLane; ++u) M = fmaxf(M, v[u].x);
+    M = warp_max(M);
+    float Ls = 0.f;
+#pragma unroll
+    for (int u = 0; u < kMergeMaxPerLane; ++u) { v[u].x = expf(v[u].x - M); Ls = fmaf(v[u].y, v[u].x, Ls); }
+    const float inv = 1.f / warp_sum(Ls);
+#pragma unroll
+    for (int u = 0; u < kMergeMaxPerLane; ++u) {
+      const int s2 = lane + 32 * u;
+      if (s2 < n_split) wsm[hq * n_split + s2] = v[u].x * inv;
+    }
+  }
+  __syncthreads();
+  trace(3, 1);
+  // o_hq = sum_s w_s o_s: thread = (split group sg of 8, float4 dims); every head's loads in flight
+  float* red = wsm + ((G * n_split + 3) & ~3);                  // [kMergeHeads][8][128]
+  const int d4 = (tid & 31) * 4, sg = tid >> 5;
+  const int nper = (n_split - sg + 7) / 8;                      // splits of this group
+#pragma unroll
+  for (int h0 = 0; h0 < G; h0 += kMergeHeads) {
+    float4 a[kMergeHeads];
+#pragma unroll
+    for (int x = 0; x < kMergeHeads; ++x) a[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u0 = 0; u0 < nper; u0 += 4) {
+      float4 vv[kMergeHeads][4];
+#pragma unroll
+      for (int x = 0; x < kMergeHeads; ++x) {
+        const size_t row = (size_t)b * D.hq + (size_t)h * G + h0 + x;
+        const float4* opr = reinterpret_cast<const float4*>(o_part + row * n_split * kHeadDim + d4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int s2 = sg + 8 * (u0 + u);
+          vv[x][u] = (u0 + u < nper && h0 + x < G) ? __ldcg(opr + (size_t)s2 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < kMergeHeads; ++x)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int s2 = sg + 8 * (u0 + u);
+          const float w = (u0 + u < nper && h0 + x < G) ? wsm[(h0 + x) * n_split + s2] : 0.f;
+          a[x].x = fmaf(w, vv[x][u].x, a[x].x); a[x].y = fmaf(w, vv[x][u].y, a[x].y);
+          a[x].z = fmaf(w, vv[x][u].z, a[x].z); a[x].w = fmaf(w, vv[x][u].w, a[x].w);
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < kMergeHeads; ++x)
+      if (h0 + x < G) *reinterpret_cast<float4*>(red + (x * 8 + sg) * kHeadDim + d4) = a[x];
+    __syncthreads();
+    for (int i = tid; i < kMergeHeads * kHeadDim; i += 256) {
+      const int x = i / kHeadDim, dd = i - x * kHeadDim;
+      if (h0 + x < G) {
+        float o = 0.f;
+#pragma unroll
+        for (int g2 = 0; g2 < 8; ++g2) o += red[(x * 8 + g2) * kHeadDim + dd];
+        out[((size_t)b * D.hq + (size_t)h * G + h0 + x) * kHeadDim + dd] = f2bf(o);
+      }
+    }
+    __syncthreads();
+  }
+  trace(2, 7);
+  if (tid == 0) counters[bh] = 0;                      // leave the workspace counter zeroed
 }
 
-__global__ void __launch_bounds__(128)
-k_combine(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_part, int n_split,
-          uint16_t* __restrict__ out) {
-  const size_t row = (size_t)blockIdx.y * D.hq + blockIdx.x;
-  const float2* ml = ml_part + row * n_split;
-  float M = -INFINITY;
-  for (int i = 0; i < n_split; ++i) M = fmaxf(M, ml[i].x);
-  float Ls = 0.f, acc = 0.f;
-  for (int i = 0; i < n_split; ++i) {
-    const float w = expf(ml[i].x - M);
-    Ls = fmaf(ml[i].y, w, Ls);
-    acc = fmaf(o_part[(row * n_split + i) * kHeadDim + threadIdx.x], w, acc);
-  }
-  out[row * kHeadDim + threadIdx.x] = f2bf(acc / Ls);
+// =============================================================================================
+// host side
+// =============================================================================================
+static int tiles_per_head(const Dims& D) { return (D.n_c + kSTile - 1) / kSTile; }
+static bool z_fits_smem(const Dims& D, int) {          // z slice in smem
+  return (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 <= kSelectSmemMax;
 }
 
-// ---------------------------------------------------------------------------------------------
 size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
-  size_t off = 0;
+  size_t off = ws_header_bytes(D);                  // zero-initialised per-(b,h) counters live first
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return base + o; };
-  const int n_sblk = (D.n_c + kScoreTile - 1) / kScoreTile;
-  const int T_max = D.o * kChunk + D.k * kChunk + D.wcap;
-  const int n_split = (T_max + kAttnTile - 1) / kAttnTile;
+  const int tph = tiles_per_head(D);
+  const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+  const int n_win_max = (D.wcap + kUnitTok - 1) / kUnitTok;
+  const int n_split = n_sel_u + n_out_u + n_win_max;
   const size_t BHq = (size_t)D.b * D.hq, BHk = (size_t)D.b * D.hk;
   char* p_log = carve(BHq * D.n_c * 4);
-  char* p_part = carve(BHq * n_sblk * 8);
-  char* p_z = carve(BHk * D.n_c * 4);
+  char* p_part = carve(BHq * tph * 4 * 8);          // per-(tile, quadrant) score partials
+  char* p_z = carve(BHk * D.n_c * 4);                // select fallback / large-n_c slices
   char* p_sel = carve(BHk * D.k * 4);
-  char* p_kt = carve(BHk * D.k * kChunk * kHeadDim * 2);
-  char* p_vt = carve(BHk * D.k * kChunk * kHeadDim * 2);
   char* p_op = carve(BHq * n_split * kHeadDim * 4);
   char* p_ml = carve(BHq * n_split * 8);
   if (ws) {
@@ -346,55 +772,117 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
     ws->part = reinterpret_cast<float2*>(p_part);
     ws->z = reinterpret_cast<float*>(p_z);
     ws->sel = reinterpret_cast<int32_t*>(p_sel);
-    ws->Kt = reinterpret_cast<uint16_t*>(p_kt);
-    ws->Vt = reinterpret_cast<uint16_t*>(p_vt);
     ws->o_part = reinterpret_cast<float*>(p_op);
     ws->ml_part = reinterpret_cast<float2*>(p_ml);
-    ws->n_sblk = n_sblk;
+    ws->counters = reinterpret_cast<int*>(base);
+    ws->n_sblk = tph;
     ws->n_split = n_split;
   }
   return off;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int G>
 static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                                    const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                                    int32_t* sel_ids, uint16_t* dbg_keys, const DecodeWs& ws,
-                                   cudaStream_t st, int* launches) {
+                                   cudaStream_t st, int* launches, Profiler* prof) {
   const float scale = (float)(1.0 / 11.313708498984761);    // 1/sqrt(d), d = 128 (R6)
-  k_score<G><<<dim3(ws.n_sblk, D.hk, D.b), 256, 0, st>>>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part,
-                                                         ws.n_sblk, scale, k_new, v_new, Ly.K_win, Ly.V_win, step);
-  k_select<G><<<dim3(D.hk, D.b), 1024, 0, st>>>(D, ws.logits, ws.part, ws.n_sblk, ws.z, ws.sel, sel_ids);
-  const size_t sm = keytile_smem_bytes(D.r);
-  cudaError_t e = cudaFuncSetAttribute(k_rebuild_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  int dev = 0, n_sm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const int n_rebuild = D.b * D.hk * ((D.k + 15) / 16);
-  k_rebuild_gather<<<n_sm + n_rebuild, kTileThreads, sm, st>>>(D, R, Ly, ws.sel, ws.Kt, ws.Vt, dbg_keys, n_sm);
-  const int T = D.o * kChunk + D.k * kChunk + D.w_eff + step + 1;
-  const int n_split_used = (T + kAttnTile - 1) / kAttnTile;
-  const size_t asm_bytes = 2 * kAttnTile * kHeadDim * 2 + G * kAttnTile * 4;
-  e = cudaFuncSetAttribute(k_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_bytes);
-  if (e != cudaSuccess) return e;
-  k_attn<G><<<dim3(n_split_used, D.hk, D.b), 128, asm_bytes, st>>>(D, Ly, q, ws.Kt, ws.Vt, step, ws.o_part,
-                                                                   ws.ml_part, n_split_used, scale);
-  k_combine<<<dim3(D.hq, D.b), 128, 0, st>>>(D, ws.o_part, ws.ml_part, n_split_used, out);
-  *launches += 5;
+  static size_t score_attr = 0;
+  static bool attrs_set = false;
+  const AttnSmem lay = attn_smem_layout(D.r, G);
+  const size_t score_smem = (size_t)kSStages * kSTile * kHeadDim * 2 + 2 * G * kSTile * 4 +
+                            (size_t)((D.n_c + 31) / 32) * 4;
+  cudaError_t e;
+  if (score_smem > score_attr) {
+    if ((e = cudaFuncSetAttribute(k_score<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem))) return e;
+    score_attr = score_smem;
+  }
+  if (!attrs_set) {
+    if ((e = cudaFuncSetAttribute(k_select<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSelectSmemMax))) return e;
+    if ((e = cudaFuncSetAttribute(k_sparse_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)attn_smem_layout(256, G).bytes))) return e;
+    attrs_set = true;
+  }
+  const int tph = ws.n_sblk;
+  const int total_tiles = D.b * D.hk * tph;
+  {
+    const int nsu = (D.k + 7) / 8, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+    const int nsp = nsu + nou + (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
+    if (nsp > 32 * kMergeMaxPerLane || (size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 > (size_t)(lay.q - lay.a))
+      return cudaErrorInvalidConfiguration;                                           // merge scratch
+  }
+  const int grid_s = total_tiles < 2 * num_sms() ? total_tiles : 2 * num_sms();
+  // a1: tcgen05 score (TMA + TMEM); CUDA-core fallback when tensor maps are unavailable
+  const char* nt = getenv("SKV_NO_TC");                 // test hook: force the CUDA-core score
+  e = (nt && nt[0] == '1') ? cudaErrorNotSupported
+                           : launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
+                                                v_new, Ly.K_win, Ly.V_win, step, num_sms(), st);
+  if (prof && e == cudaSuccess) profile_mark(prof, kScore, false, st);
+  if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
+    cudaGetLastError();
+    if (prof) profile_mark(prof, kScore, false, st);
+    k_score<G><<<grid_s, 256, score_smem, st>>>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
+                                                v_new, Ly.K_win, Ly.V_win, step);
+    e = cudaGetLastError();
+  }
+  if (e) return e;
+  if (prof) { profile_mark(prof, kScore, true, st); profile_mark(prof, kSelect, false, st); }
+  {
+    const bool zsm = z_fits_smem(D, G);
+    const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
+    if (zsm) e = launch_pdl(k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
+                            (const float*)ws.logits, (const float2*)ws.part, tph * 4, ws.z, ws.sel, sel_ids);
+    else e = launch_pdl(k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
+                        (const float*)ws.logits, (const float2*)ws.part, tph * 4, ws.z, ws.sel, sel_ids);
+    if (e) return e;
+    if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
+  }
+  const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+  const int n_win_u = (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
+  const int n_split = n_sel_u + n_out_u + n_win_u;
+  const int units = D.b * D.hk * n_split;
+  if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
+                      (const int32_t*)ws.sel, step, ws.o_part, ws.ml_part, n_sel_u, n_out_u, n_win_u, n_split, scale,
+                      dbg_keys, ws.counters, out))) return e;
+  if (prof) profile_mark(prof, kSparseAttn, true, st);
+  *launches += 3;
   return cudaGetLastError();
 }
 
 cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                           const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                           int32_t* sel_ids, uint16_t* dbg_keys, const DecodeWs& ws, cudaStream_t st,
-                          int* launches) {
+                          int* launches, Profiler* prof) {
   switch (D.g) {
-    case 1: return launch_decode_g<1>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches);
-    case 2: return launch_decode_g<2>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches);
-    case 4: return launch_decode_g<4>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches);
-    case 8: return launch_decode_g<8>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches);
-    case 16: return launch_decode_g<16>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches);
+    case 1: return launch_decode_g<1>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof);
+    case 2: return launch_decode_g<2>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof);
+    case 4: return launch_decode_g<4>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof);
+    case 8: return launch_decode_g<8>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof);
+    case 16: return launch_decode_g<16>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof);
   }
   return cudaErrorInvalidValue;
 }

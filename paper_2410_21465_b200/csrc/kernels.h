@@ -31,22 +31,42 @@ struct BuildWs {
   float* negm;       // [b][hk][n_c]  (-m, keys for the outlier top-o)
 };
 struct DecodeWs {
+  int* counters;     // [b][hk] zero-initialised by the caller once; every call leaves them zero
   float* logits;     // [b][hq][n_c]
-  float2* part;      // [b][hq][n_sblk]  softmax partials (max, sumexp)
-  float* z;          // [b][hk][n_c]
+  float2* part;      // [b][hq][n_part]  per-(tile, quadrant) softmax partials (max, sumexp)
+  float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
   int32_t* sel;      // [b][hk][k]
-  uint16_t* Kt;      // [b][hk][k*c][d]
-  uint16_t* Vt;      // [b][hk][k*c][d]
   float* o_part;     // [b][hq][n_split][d]
   float2* ml_part;   // [b][hq][n_split]
   int n_sblk, n_split;
 };
 
-constexpr int kScoreTile = 256;   // chunks per score block
-constexpr int kAttnTile = 128;    // tokens per attention split
+constexpr int kSTile = 128;                       // landmark rows per score tile (32 KB)
+constexpr int kSStages = 3;                       // score smem ring depth (2 CTAs / SM)
+constexpr int kUnitTok = 64;                      // tokens per attention unit (8 chunks)
+constexpr size_t kSelectSmemMax = 160 * 1024;     // per-CTA z slice + its logits kept in smem
+constexpr int kSelCL = 8;                         // select: CTAs per (request, KV head) cluster
+constexpr int kSelThreads = 512;
+constexpr int kSelCandLocal = 1024;               // threshold-bucket candidates per CTA
 
+inline size_t ws_header_bytes(const Dims& D) { return ((size_t)D.b * D.hk * 4 + 255) & ~(size_t)255; }
 size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base);
 size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base);
+
+// Optional per-kernel CUDA-event timing (shadowkv_profile_*): kernel ids below.
+enum KernelId { kScore = 0, kSelect = 1, kSparseAttn = 2, kReserved = 3, kCombine = 4, kNumKernelIds = 5 };
+struct Profiler;                                            // defined in abi.cu
+void profile_mark(Profiler* p, int kernel, bool end, cudaStream_t st);
+
+cudaError_t set_trace_buffer(void* dev_ptr);      // decode.cu: nullptr disables
+cudaError_t set_trace_buffer_tc(void* dev_ptr);   // score_tc.cu (kernel slot 0)
+
+// score_tc.cu: tcgen05 landmark scoring (a1); cudaErrorNotSupported if tensor maps are unavailable
+template <int G>
+cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
+                            float* logits, float2* part, int tiles_per_head, float scale,
+                            const uint16_t* k_new, const uint16_t* v_new, uint16_t* K_win, uint16_t* V_win,
+                            int step, int n_sm, cudaStream_t st);
 
 // each returns cudaGetLastError() after its launches and adds to *launches
 cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* K_rope,
@@ -54,6 +74,6 @@ cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const ui
 cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                           const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                           int32_t* sel_ids, uint16_t* dbg_keys, const DecodeWs& ws, cudaStream_t st,
-                          int* launches);
+                          int* launches, Profiler* prof);
 
 }  // namespace skv

@@ -1,0 +1,356 @@
+// a1 landmark scoring on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+//   P = Q . L^T / sqrt(d)   (Alg 2 "P <- MatMul(Q, L^T)"; scale R6)
+//
+// One UMMA per 16-wide k step: M = 128 landmark rows (A, K-major, SWIZZLE_128B, streamed from HBM
+// by TMA in two 64-column boxes), N = 16 query heads of the GQA group (B, zero-padded, built once
+// per KV head in smem), K = 128 = head_dim, fp32 accumulators in TMEM (2 x 16 columns, double
+// buffered).  Warp roles (192 threads): warps 0-3 epilogue (TMEM lane quadrant = warp), warp 4
+// TMA producer, warp 5 MMA issuer.  The epilogue reads each landmark's G logits with tcgen05.ld,
+// masks outlier chunks (R3), writes the scaled logits and a per-(tile, quadrant) softmax partial
+// (max, sum exp) that k_select merges into the exact per-head log-sum-exp.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace skv {
+
+namespace {
+
+constexpr int kTcStages = 6;
+constexpr int kTcAcc = 8;                 // TMEM accumulator buffers (16 fp32 columns each)
+constexpr int kTcMaxHeads = 4;            // KV heads a CTA's contiguous tile range may touch
+constexpr int kTcMaxTiles = 64;           // tiles per CTA (bitmap size); host sizes the grid accordingly
+constexpr int kTcThreads = 192;
+constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
+constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);          // start address      [0,14)
+  d |= (uint64_t)1u << 16;                          // LBO (unused for swizzled K-major) [16,30)
+  d |= (uint64_t)(1024u >> 4) << 32;                // SBO = 1024 B       [32,46)
+  d |= (uint64_t)1u << 46;                          // version = 1 (Blackwell) [46,48)
+  d |= (uint64_t)2u << 61;                          // layout = SWIZZLE_128B   [61,64)
+  return d;
+}
+
+// kind::f16 instruction descriptor: A,B bf16 K-major, D fp32, M = 128, N = 16.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      :: "r"(dtmem), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ bool in_sorted(const int32_t* ids, int o, int j) {
+  int lo = 0, hi = o;
+  while (lo < hi) { int mid = (lo + hi) >> 1; if (ids[mid] < j) lo = mid + 1; else hi = mid; }
+  return lo < o && ids[lo] == j;
+}
+
+__device__ uint64_t* g_trace_tc = nullptr;              // same layout as decode.cu's trace buffer
+__device__ __forceinline__ void trace_tc(uint64_t* t, int ev) {
+  if (t != nullptr && threadIdx.x == 0) t[(size_t)blockIdx.x * 8 + ev] = globaltimer();
+}
+__device__ __forceinline__ void trace_tc_any(uint64_t* t, int ev) {   // caller restricts to one thread
+  if (t != nullptr) t[(size_t)blockIdx.x * 8 + ev] = globaltimer();
+}
+
+}  // namespace
+
+cudaError_t set_trace_buffer_tc(void* p) { return cudaMemcpyToSymbol(g_trace_tc, &p, sizeof(void*)); }
+
+template <int G>
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __restrict__ oids,
+           const uint16_t* __restrict__ q, float* __restrict__ logits, float2* __restrict__ part,
+           int tiles_per_head, float scale, const uint16_t* __restrict__ k_new,
+           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step) {
+  static_assert(G <= 16, "N = 16 covers the GQA group");
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint8_t* sA = smem;                                          // [stages][32 KB]
+  uint8_t* sB = smem + kTcStages * kTileBytes;                 // [kTcMaxHeads][4 KB]
+  __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], acc_full[kTcAcc], acc_empty[kTcAcc];
+  __shared__ uint32_t tmem_base;
+  __shared__ uint32_t obits[kTcMaxTiles * (kSTile / 32)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = D.b * D.hk * tiles_per_head;
+  const int t_begin = (int)((long long)blockIdx.x * total / gridDim.x);
+  const int t_end = (int)((long long)(blockIdx.x + 1) * total / gridDim.x);
+  const int ntile = t_end - t_begin;
+  const int bh0 = t_begin / tiles_per_head;
+  uint64_t* const trace_buf = g_trace_tc;
+  trace_tc(trace_buf, 0);
+  pdl_trigger();
+  // the producer thread initialises the barriers and puts the first kTcStages tiles in flight
+  // before anything else, so HBM streaming starts at kernel entry
+  if (tid == 4 * 32 && ntile > 0) {
+    for (int s = 0; s < kTcStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kTcAcc; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    for (int i = 0; i < ntile && i < kTcStages; ++i) {
+      const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
+      const int row0 = bh * D.n_c + tile * kSTile;
+      mbar_expect_tx(&full[i], kTileBytes);
+      tma_load_2d(sA + i * kTileBytes, &tmap, 0, row0, &full[i]);
+      tma_load_2d(sA + i * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[i]);
+    }
+  }
+  if (ntile <= 0) return;
+  if (warp == 0) {                                     // TMEM: 2 buffers x 4 chains x 16 fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" :: "r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const int nheads = (t_end - 1) / tiles_per_head - bh0 + 1;          // <= kTcMaxHeads (host check)
+  // setup with every global load issued before any dependent use:
+  //   B operands (q of each KV head in range, K-major SWIZZLE_128B, rows n >= G zero),
+  //   outlier bitmap of this CTA's landmark rows (R3), a7 window append (R18)
+  constexpr int kBChunks = kTcMaxHeads * 16 * 16;
+  uint4 qv[(kBChunks + kTcThreads - 1) / kTcThreads];
+#pragma unroll
+  for (int u = 0; u < (kBChunks + kTcThreads - 1) / kTcThreads; ++u) {
+    const int i = tid + u * kTcThreads;
+    const int hi = i >> 8, n = (i >> 4) & 15, ch = i & 15;
+    qv[u] = make_uint4(0, 0, 0, 0);
+    if (i < nheads * 256 && n < G) {
+      const int bh = bh0 + hi, b = bh / D.hk, h = bh - b * D.hk;
+      qv[u] = *reinterpret_cast<const uint4*>(q + ((size_t)b * D.hq + (size_t)h * G + n) * kHeadDim + ch * 8);
+    }
+  }
+  int oid = -1, obh = 0;
+  if (tid < nheads * D.o && D.o > 0) { obh = bh0 + tid / D.o; oid = oids[(size_t)obh * D.o + tid % D.o]; }
+  const int row_begin = t_begin * kSTile;
+  for (int w = tid; w < ntile * (kSTile / 32); w += kTcThreads) obits[w] = 0u;
+#pragma unroll
+  for (int u = 0; u < (kBChunks + kTcThreads - 1) / kTcThreads; ++u) {
+    const int i = tid + u * kTcThreads;
+    if (i < nheads * 256) {
+      const int hi = i >> 8, n = (i >> 4) & 15, ch = i & 15;
+      const int sub = ch >> 3, c16 = ch & 7;
+      *reinterpret_cast<uint4*>(sB + hi * kBBytes + sub * 2048 + n * 128 + ((c16 ^ (n & 7)) << 4)) = qv[u];
+    }
+  }
+  for (int idx = blockIdx.x * kTcThreads + tid; idx < D.b * D.hk * 32; idx += gridDim.x * kTcThreads) {
+    const int bh = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;
+    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + step) * kHeadDim + p * 8;
+    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bh * kHeadDim + p * 8;
+    *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
+  }
+  trace_tc(trace_buf, 6);
+  __syncthreads();
+  if (oid >= 0) {
+    const int tr = obh * tiles_per_head * kSTile + oid - row_begin;   // row in this CTA's tile space
+    if (tr >= 0 && tr < ntile * kSTile) atomicOr(&obits[tr >> 5], 1u << (tr & 31));
+  }
+  for (int i = kTcThreads + tid; i < nheads * D.o; i += kTcThreads) {    // (o > 48 per head: rare)
+    const int bh = bh0 + i / D.o, j = oids[(size_t)bh * D.o + i % D.o];
+    const int tr = bh * tiles_per_head * kSTile + j - row_begin;
+    if (tr >= 0 && tr < ntile * kSTile) atomicOr(&obits[tr >> 5], 1u << (tr & 31));
+  }
+  fence_proxy_async();                                    // B (generic writes) -> UMMA (async proxy)
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  trace_tc(trace_buf, 7);                                         // setup done
+
+  if (warp == 4) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int i = kTcStages; i < ntile; ++i) {
+        const int s = i % kTcStages, ph = (i / kTcStages) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
+        const int row0 = bh * D.n_c + tile * kSTile;
+        mbar_expect_tx(&full[s], kTileBytes);
+        tma_load_2d(sA + s * kTileBytes, &tmap, 0, row0, &full[s]);
+        tma_load_2d(sA + s * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[s]);
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------- MMA issuer (single thread) ----------------
+    if (lane == 0) {
+      for (int i = 0; i < ntile; ++i) {
+        const int s = i % kTcStages, ph = (i / kTcStages) & 1, buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
+        mbar_wait(&full[s], ph);
+        if (i < 4) trace_tc_any(trace_buf, 2 + i);                  // tile i landed in smem
+        mbar_wait(&acc_empty[buf], aph ^ 1);
+        tc_fence_after();
+        const int hi = (t_begin + i) / tiles_per_head - bh0;
+        const uint32_t a0 = smem_u32(sA + s * kTileBytes), b0 = smem_u32(sB + hi * kBBytes);
+#pragma unroll
+        for (int k = 0; k < kHeadDim / 16; ++k) {
+          const uint32_t koff = (k >> 2) * (kTileBytes / 2) + (k & 3) * 32;
+          const uint32_t kboff = (k >> 2) * 2048 + (k & 3) * 32;
+          umma_f16(tmem + buf * 16, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + kboff), k > 0);
+        }
+        umma_commit(&empty[s]);          // smem stage may be refilled once these MMAs retire
+        umma_commit(&acc_full[buf]);     // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 0-3, TMEM lanes 32w .. 32w+31 ----------------
+    // per-thread online softmax partials over the CTA's rows of each KV head; one warp reduction
+    // per head segment (slot = first tile of the segment; the segment's other slots are emptied)
+    const int nq = tiles_per_head * 4;                    // partial slots per (b, q head)
+    float m_run[G], s_run[G];
+#pragma unroll
+    for (int hq = 0; hq < G; ++hq) { m_run[hq] = -INFINITY; s_run[hq] = 0.f; }
+    int cur_bh = t_begin / tiles_per_head, first_tile = t_begin - cur_bh * tiles_per_head;
+    auto flush = [&](int bh, int slot_tile) {
+      const int b = bh / D.hk, h = bh - b * D.hk;
+#pragma unroll
+      for (int hq = 0; hq < G; ++hq) {
+        const float m = warp_max(m_run[hq]);
+        const float sc = (m > -INFINITY && m_run[hq] > -INFINITY) ? s_run[hq] * expf(m_run[hq] - m) : 0.f;
+        const float sm = warp_sum(sc);
+        if (lane == hq) part[((size_t)b * D.hq + (size_t)h * G + hq) * nq + slot_tile * 4 + warp] = make_float2(m, sm);
+        m_run[hq] = -INFINITY; s_run[hq] = 0.f;
+      }
+    };
+    for (int i = 0; i < ntile; ++i) {
+      const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
+      const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
+      if (bh != cur_bh) { flush(cur_bh, first_tile); cur_bh = bh; first_tile = tile; }
+      const int b = bh / D.hk, h = bh - b * D.hk;
+      mbar_wait(&acc_full[buf], aph);
+      tc_fence_after();
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + buf * 16, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      const int r = 32 * warp + lane, j = tile * kSTile + r;
+      const bool out = (obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u;
+      if (j < D.n_c) {
+        float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c + j;
+#pragma unroll
+        for (int hq = 0; hq < G; ++hq) {
+          const float x = out ? -INFINITY : v[hq] * scale;
+          lb[(size_t)hq * D.n_c] = x;
+          if (x > m_run[hq]) { s_run[hq] = s_run[hq] * expf(m_run[hq] - x) + 1.f; m_run[hq] = x; }
+          else if (x > -INFINITY) s_run[hq] += expf(x - m_run[hq]);
+        }
+      }
+      if (tile != first_tile && lane < G)
+        part[((size_t)b * D.hq + (size_t)h * G + lane) * nq + tile * 4 + warp] = make_float2(-INFINITY, 0.f);
+    }
+    flush(cur_bh, first_tile);
+  }
+  __syncthreads();
+  trace_tc(trace_buf, 1);
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" :: "r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host: tensor map over the landmark matrix viewed as [b*h_kv*n_c rows][128] bf16
+// ---------------------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+size_t score_tc_smem_bytes() { return 1024 + (size_t)kTcStages * kTileBytes + (size_t)kTcMaxHeads * kBBytes; }
+
+int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm) {
+  const int total = D.b * D.hk * tiles_per_head;
+  int grid = total < n_sm ? total : n_sm;
+  // each CTA's contiguous tile range must touch at most kTcMaxHeads KV heads and kTcMaxTiles tiles
+  while (grid < total && ((total + grid - 1) / grid > (kTcMaxHeads - 1) * tiles_per_head ||
+                          (total + grid - 1) / grid > kTcMaxTiles))
+    grid = grid * 2 < total ? grid * 2 : total;
+  return grid;
+}
+
+template <int G>
+cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
+                            float* logits, float2* part, int tiles_per_head, float scale,
+                            const uint16_t* k_new, const uint16_t* v_new, uint16_t* K_win, uint16_t* V_win,
+                            int step, int n_sm, cudaStream_t st) {
+  auto enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t gdim[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)D.b * D.hk * D.n_c};
+  const cuuint64_t gstride[1] = {(cuuint64_t)kHeadDim * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)kSTile};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(L), gdim, gstride, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  cudaError_t e;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(k_score_tc<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)score_tc_smem_bytes()))) return e;
+    attr = true;
+  }
+  const int grid = score_tc_grid(D, tiles_per_head, n_sm);
+  k_score_tc<G><<<grid, kTcThreads, score_tc_smem_bytes(), st>>>(map, D, oids, q, logits, part, tiles_per_head,
+                                                                scale, k_new, v_new, K_win, V_win, step);
+  return cudaGetLastError();
+}
+
+#define SKV_INST(G)                                                                                       \
+  template cudaError_t launch_score_tc<G>(const Dims&, const uint16_t*, const int32_t*, const uint16_t*,  \
+                                          float*, float2*, int, float, const uint16_t*, const uint16_t*,  \
+                                          uint16_t*, uint16_t*, int, int, cudaStream_t);
+SKV_INST(1)
+SKV_INST(2)
+SKV_INST(4)
+SKV_INST(8)
+SKV_INST(16)
+#undef SKV_INST
+
+}  // namespace skv

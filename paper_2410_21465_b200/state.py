@@ -50,7 +50,7 @@ class Shape:
 
 def alloc_workspace(shape: Shape, device="cuda") -> torch.Tensor:
     n = bd.shadowkv_workspace_bytes(shape.dims())
-    return torch.empty(n + 256, dtype=torch.uint8, device=device)
+    return torch.zeros(n + 256, dtype=torch.uint8, device=device)     # ABI: zero-filled before first use
 
 
 def ws_ptr(ws: torch.Tensor) -> int:

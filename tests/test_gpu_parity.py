@@ -80,6 +80,20 @@ def test_decode_parity_identical_state(name, seed):
         np.testing.assert_array_equal(f64(P.st.V_win[:, :, slot]), f64(si["v_new"]))
 
 
+@pytest.mark.parametrize("name", ["c1", "glm_g16_interleaved", "g1_batch2", "multi_tile_k"])
+def test_decode_parity_cuda_core_score(name, monkeypatch):
+    """Same parity check with the CUDA-core score kernel (fallback when TMA tensor maps are unavailable)."""
+    monkeypatch.setenv("SKV_NO_TC", "1")
+    P = Problem(CASES[name], seed=4, steps=2)
+    ost = P.oracle_build()
+    P.load_state_from_oracle(ost)
+    for step in range(2):
+        si = P.step_inputs(step)
+        gout, gsel, gkeys = P.gpu_decode(step, si)
+        oout, osel, oz, okeys, ost = P.oracle_decode(ost, step, si)
+        check_decode(P.cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
+
+
 @pytest.mark.parametrize("name", ["c1", "glm_g16_interleaved", "g8_ragged"])
 def test_end_to_end_build_then_decode(name):
     """GPU build -> GPU decode vs oracle build -> oracle decode (states may differ by 1 bf16 ulp)."""

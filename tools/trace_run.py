@@ -1,0 +1,59 @@
+"""Per-CTA timeline of one decode layer (globaltimer stamps, see shadowkv_trace_buffer).
+
+python tools/trace_run.py [--config c2] [--layers 4]  -> prints phase statistics (us, relative to
+the score kernel's first CTA) for score / select / sparse-attn CTAs of the last traced layer."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace, binding as bd  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--layers", type=int, default=4)
+args = ap.parse_args()
+cfg = synth.CONFIGS[args.config]
+shape = Shape.from_config(cfg, steps=64)
+inv, rot, il = synth.rope_table(cfg)
+rope = RopeTable(inv, rot, il)
+ws = alloc_workspace(shape)
+states = []
+for l in range(args.layers):
+    inp = synth.gen_layer(cfg, 99, layer=l, device="cuda")
+    st = LayerState(shape)
+    st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
+    st.build(rope.struct, ws)
+    states.append(st)
+out = torch.empty(cfg.batch, cfg.n_q_heads, 128, dtype=torch.bfloat16, device="cuda")
+tr = torch.zeros(4 * 4096 * 8, dtype=torch.int64, device="cuda")
+for step in range(6):
+    for l, st in enumerate(states):
+        si = synth.gen_step(cfg, 99, l, step, device="cuda")
+        if step == 5 and l == args.layers - 1:
+            torch.cuda.synchronize()
+            tr.zero_()
+            bd.shadowkv_trace_buffer(tr)
+        st.decode(rope.struct, si["q"], si["k_new"], si["v_new"], step, out, ws)
+        if step == 5 and l == args.layers - 1:
+            torch.cuda.synchronize()
+            bd.shadowkv_trace_buffer(None)
+t = tr.view(4, 4096, 8).cpu().numpy().astype(np.float64)
+t0 = t[0][t[0][:, 0] > 0][:, 0].min()
+names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand", "sync2", "end"],
+         3: ["merge_start", "weights"],
+         2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end"]}
+for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
+    m = t[kid]
+    rows = m[m[:, 0] > 0]
+    print(f"== {kn}: {len(rows)} CTAs")
+    for e, en in enumerate(names[kid]):
+        col = rows[:, e]
+        col = col[col > 0]
+        if len(col):
+            r = (col - t0) / 1e3
+            print(f"   {en:14s} n={len(r):4d} min={r.min():8.2f} p50={np.median(r):8.2f} p90={np.percentile(r, 90):8.2f} max={r.max():8.2f} us")
