@@ -150,8 +150,8 @@ SKV_API int32_t shadowkv_last_launch_count(void);
  * the summed milliseconds and launch counts per id into total_ms[5] / counts[5] (nullable) and
  * destroys the events.  Not thread-safe; one profiling session per process. */
 SKV_API skv_status shadowkv_profile_begin(int32_t capacity, int32_t kernel_mask);
-/* Tuning aid: when dev_buf (device, >= 4*4096*8 uint64) is non-NULL, decode kernels write
- * %globaltimer stamps [0 score | 1 select | 2 sparse-attn | 3 merge][CTA < 4096][event < 8] into it.
+/* Tuning aid: when dev_buf (device, >= 4*4096*16 uint64) is non-NULL, decode kernels write
+ * %globaltimer stamps [0 score | 1 select | 2 sparse-attn | 3 merge][CTA < 4096][event < 16] into it.
  * NULL (the default) disables the stamps. */
 SKV_API skv_status shadowkv_trace_buffer(void *dev_buf);
 SKV_API skv_status shadowkv_profile_end(double *total_ms, int32_t *counts);

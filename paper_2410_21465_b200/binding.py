@@ -152,5 +152,5 @@ def shadowkv_profile_end():
 
 
 def shadowkv_trace_buffer(buf):
-    """Enable (device tensor of >= 4*4096*8 int64) or disable (None) the kernels' globaltimer stamps."""
+    """Enable (device tensor of >= 4*4096*16 int64) or disable (None) the kernels' globaltimer stamps."""
     _check(load().shadowkv_trace_buffer(_ptr(buf)))

@@ -29,14 +29,14 @@ constexpr int kMergeMaxPerLane = 16;   // merge handles n_split <= 512 partial u
 constexpr int kMergeHeads = 4;         // heads whose partial loads are in flight together
 
 
-// optional per-CTA timeline (globaltimer ns) for tuning: [kernel][block < 4096][event < 8]
+// optional per-CTA timeline (globaltimer ns) for tuning: [kernel][block < 4096][event < 16]
 __device__ uint64_t* g_trace = nullptr;
 // kernels read g_trace once (TRACE_INIT) so that disabled tracing costs no dependent loads
 #define TRACE_INIT uint64_t* const trace_buf_ = g_trace
 #define trace(kernel, ev)                                                                            \
   do {                                                                                               \
     if (trace_buf_ != nullptr && threadIdx.x == 0)                                                   \
-      trace_buf_[((size_t)(kernel) * 4096 + blockIdx.x) * 8 + (ev)] = globaltimer();                 \
+      trace_buf_[((size_t)(kernel) * 4096 + blockIdx.x) * 16 + (ev)] = globaltimer();                \
   } while (0)
 cudaError_t set_trace_buffer(void* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof(void*)); }
 
@@ -143,6 +143,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
   if (tid == 0)
     for (int it = 0; it < kSStages - 1; ++it) issue(it);
   float qr[G][8];
+  float seg_m[2] = {-INFINITY, -INFINITY}, seg_s[2] = {0.f, 0.f};   // running partial of heads warp, warp+8
   int cur_bh = -1;
   for (int it = 0; t_begin + it < t_end; ++it) {
     const int t = t_begin + it;
@@ -189,7 +190,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
       const int hq = idx / kSTile, r = idx - hq * kSTile;
       if (r < rows) lb[(size_t)hq * D.n_c + r] = Pb[idx];
     }
-    for (int hq = warp; hq < G; hq += 8) {           // tile softmax partial in slot 4*tile, 3 empty slots
+    for (int hq = warp; hq < G; hq += 8) {           // tile softmax partial merged into the segment's
       float x[kSTile / 32];
       float m = -INFINITY;
 #pragma unroll
@@ -201,8 +202,14 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
         for (int u = 0; u < kSTile / 32; ++u) sm += expf(x[u] - m);
       }
       sm = warp_sum(sm);
-      float2* pp = part + ((size_t)b * D.hq + (size_t)h * G + hq) * (tiles_per_head * 4) + tile * 4;
-      if (lane < 4) pp[lane] = lane == 0 ? make_float2(m, sm) : make_float2(-INFINITY, 0.f);
+      lse_merge(seg_m[hq >> 3], seg_s[hq >> 3], m, sm);
+      const bool last_of_seg = (it + 1 == t_end - t_begin) || ((t + 1) / tiles_per_head != bh);
+      if (last_of_seg) {
+        if (lane == 0)
+          part[((size_t)b * D.hq + (size_t)h * G + hq) * kSegMax +
+               ((int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x))] = make_float2(seg_m[hq >> 3], seg_s[hq >> 3]);
+        seg_m[hq >> 3] = -INFINITY; seg_s[hq >> 3] = 0.f;
+      }
     }
   }
   trace(0, 1);
@@ -233,18 +240,20 @@ __device__ __forceinline__ int block_sum(int x, int* wsum) {
 
 template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 1)
-k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int n_part,
-         float* __restrict__ zws, int32_t* __restrict__ sel, int32_t* __restrict__ sel_user) {
+k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
+         int score_total, int score_grid, float* __restrict__ zws, int32_t* __restrict__ sel,
+         int32_t* __restrict__ sel_user, int early_trigger) {
   TRACE_INIT;
   constexpr int NT = kSelThreads, NW = NT / 32;
   extern __shared__ __align__(16) float zdyn[];
   __shared__ TopKSmem<NT> tk;
-  __shared__ float lse[G], hm[G], wred[NW][G], wred2[NW][G];
-  __shared__ int hist[256], ghist[256], below[kSelCL], taken_r[kSelCL], info[4];
+  __shared__ float lse[G], hm[G];
+  __shared__ int hist[256], ghist[256], below[kSelCL], info[4];
   __shared__ int cidx[kSelCandLocal], ccnt;
   __shared__ uint32_t ckey[kSelCandLocal];
-  __shared__ int aidx[kSelCandLocal], arank[kSelCandLocal];
+  __shared__ int aidx[kSelCandLocal];
   __shared__ uint32_t akey[kSelCandLocal];
+  __shared__ int tks[kSelCandLocal], tkf[kSelCandLocal];
   __shared__ int wtmp[NW * kSelCL], wcnt[NW * 64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t crank = cluster_ctarank();
@@ -257,48 +266,55 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * n + lo;
   int32_t* out = sel + bh * k;
   trace(1, 0);
-  pdl_trigger();                                        // sparse-attn CTAs may start their prologue
+  if (early_trigger) pdl_trigger();                     // sparse-attn CTAs may start their prologue
   for (int i = tid; i < 256; i += NT) hist[i] = 0;
-  if (tid < kSelCL) taken_r[tid] = 0;
   if (tid == 0) { ccnt = 0; info[0] = info[1] = 0; }
   pdl_wait();
   trace(1, 1);
-  // ---- lse_hq from the score kernel's partials: NW/G warps per head, fixed-order online merges
-  {
-    const int wph = NW / G > 0 ? NW / G : 1;           // warps per head
-    for (int hq = warp / wph; hq < G; hq += NW / wph) {
-      const int wi = warp % wph;
-      const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + hq) * n_part;
-      float m = -INFINITY, sm = 0.f;
-      for (int i = wi * 32 + lane; i < n_part; i += wph * 32) { const float2 v = ph[i]; lse_merge(m, sm, v.x, v.y); }
-#pragma unroll
-      for (int msk = 16; msk > 0; msk >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m, msk), s2 = __shfl_xor_sync(0xffffffffu, sm, msk);
-        lse_merge(m, sm, m2, s2);
-      }
-      if (lane == 0) wred[wi][hq] = m, wred2[wi][hq] = sm;
-    }
-    __syncthreads();
-    if (tid < G) {
-      float m = -INFINITY, sm = 0.f;
-      for (int wi = 0; wi < wph; ++wi) lse_merge(m, sm, wred[wi][tid], wred2[wi][tid]);
-      lse[tid] = m + logf(sm);
-      hm[tid] = m;
-    }
-    __syncthreads();
+  // ---- lse_hq from the score CTAs' per-segment partials: max-reduce, one exp per lane, sum-reduce
+  //      (short dependent chains; fixed order, deterministic)
+  if (warp < G) {
+    const int nseg = seg_count((int)bh, tiles_per_head, score_total, score_grid);
+    if (warp == 0) trace(1, 13);
+    const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * kSegMax;
+    float2 v0 = lane < nseg ? ph[lane] : make_float2(-INFINITY, 0.f);
+    float2 v1 = lane + 32 < nseg ? ph[lane + 32] : make_float2(-INFINITY, 0.f);   // nseg <= kSegMax = 64
+    const float m = warp_max(fmaxf(v0.x, v1.x));
+    if (warp == 0) trace(1, 14);
+    float e = 0.f;
+    if (v0.x > -INFINITY) e += v0.y * expf(v0.x - m);
+    if (v1.x > -INFINITY) e += v1.y * expf(v1.x - m);
+    const float sm = warp_sum(e);
+    if (lane == 0) { lse[warp] = m + logf(sm); hm[warp] = m; }
+    if (warp == 0) trace(1, 15);
   }
+  __syncthreads();
   // max_j z_j = max_g (max_j l_gj - lse_g): known from the partials, no extra pass
   float zmax = -INFINITY;
 #pragma unroll
   for (int hq = 0; hq < G; ++hq) zmax = fmaxf(zmax, hm[hq] - lse[hq]);
   trace(1, 2);
   // ---- z = max_g (l - lse) on the slice (R4, R5) + bucket histogram
-  for (int j = tid; j < len; j += NT) {
-    float zz = -INFINITY;
+  constexpr int U = G >= 8 ? 1 : 4;
+  for (int j0 = 0; j0 < len; j0 += U * NT) {
+    float lg[U][G];
 #pragma unroll
-    for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lb[(size_t)hq * n + j] - lse[hq]);
-    z[j] = zz;
-    if (zz > -INFINITY) atomicAdd(&hist[zbucket(zz, zmax)], 1);
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * NT + tid;
+#pragma unroll
+      for (int hq = 0; hq < G; ++hq) lg[u][hq] = j < len ? lb[(size_t)hq * n + j] : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * NT + tid;
+      float zz = -INFINITY;
+#pragma unroll
+      for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lg[u][hq] - lse[hq]);
+      if (j < len) {
+        z[j] = zz;
+        if (zz > -INFINITY) atomicAdd(&hist[zbucket(zz, zmax)], 1);
+      }
+    }
   }
   trace(1, 3);
   cluster_sync_all();                                                   // #1 histograms published
@@ -332,24 +348,37 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   }
   __syncthreads();
   const int B = info[0], need = info[1];
-  // per-rank count of elements strictly above the threshold bucket
+  // per-rank count of elements strictly above the threshold bucket (the "definite" selections)
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) {
     const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
     if (lane == 0) wtmp[warp * kSelCL + r] = v;
   }
-  bool fallback = B == 255;
+  bool fallback = B == 255 || n_per > 16384;
+  const int rounds = (len + NT - 1) / NT;                             // <= 32 when n_per <= 16384
   if (!fallback) {
-    for (int j = tid; j < len; j += NT) {
-      const float zz = z[j];
-      if (zz > -INFINITY && zbucket(zz, zmax) == B) {
+    // one pass: threshold-bucket candidates + per-(round, warp) counts of definite elements
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int j = rd * NT + tid;
+      int bk = 256;
+      float zz = -INFINITY;
+      if (j < len) { zz = z[j]; if (zz > -INFINITY) bk = zbucket(zz, zmax); }
+      if (bk == B) {
         const int pos = atomicAdd(&ccnt, 1);
         if (pos < kSelCandLocal) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
       }
+      const unsigned bal = __ballot_sync(0xffffffffu, bk < B);
+      if (lane == 0) wcnt[rd * NW + warp] = __popc(bal);
     }
   }
   __syncthreads();
   if (tid < kSelCL) { int t = 0; for (int w = 0; w < NW; ++w) t += wtmp[w * kSelCL + tid]; below[tid] = t; }
+  if (!fallback) {                                      // exclusive scan of the definite counts
+    int tot;
+    const int mine = tid < rounds * NW ? wcnt[tid] : 0;
+    const int ex = block_exclusive_scan<NT>(mine, tk, &tot);
+    if (tid < rounds * NW) wcnt[tid] = ex;
+  }
   trace(1, 5);
   cluster_sync_all();                                                   // #2 candidates published
   trace(1, 6);
@@ -358,9 +387,10 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   for (int r = 0; r < kSelCL; ++r) rc[r] = fallback ? 0 : ld_dsmem_i32(dsmem_addr(&ccnt, r));
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); }
-  fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal || n_per > 16384;
+  fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal;
   if (!fallback) {
-    // all ranks' candidates -> local smem, then rank: larger z first, ties -> lower index (R12)
+    // all ranks' candidates -> local smem; the taken ones (rank < need, larger z first, ties -> lower
+    // index, R12) form a sorted index list used to place every selection
     for (int t = tid; t < total; t += NT) {
       int r = 0, base = 0;
 #pragma unroll
@@ -368,49 +398,59 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       const int c = t - base;
       aidx[t] = ld_dsmem_i32(dsmem_addr(&cidx[c], r));
       akey[t] = (uint32_t)ld_dsmem_i32(dsmem_addr(&ckey[c], r));
-      arank[t] = r;
     }
     __syncthreads();
+    trace(1, 8);
     for (int t = tid; t < total; t += NT) {
       const uint32_t u = akey[t];
       const int j = aidx[t];
       int rank = 0;
+#pragma unroll 8
       for (int c = 0; c < total; ++c) rank += (akey[c] > u) || (akey[c] == u && aidx[c] < j);
-      const bool take = rank < need;
-      if (take) atomicAdd(&taken_r[arank[t]], 1);
-      if (arank[t] == (int)crank) z[j - lo] = take ? INFINITY : -INFINITY;
+      tkf[t] = rank < need;
     }
     __syncthreads();
-    int base = 0;
-    for (int r = 0; r < (int)crank; ++r) base += below[r] + taken_r[r];
-    // ---- emit this slice ascending (a3 output)
-    const int rounds = (len + NT - 1) / NT;                           // <= 64 (n_per <= 32768)
+    for (int t = tid; t < total; t += NT) {
+      if (!tkf[t]) continue;
+      const int j = aidx[t];
+      int ord = 0;                                       // position among the taken, by index
+#pragma unroll 8
+      for (int c = 0; c < total; ++c) ord += tkf[c] && aidx[c] < j;
+      tks[ord] = j;
+      if (j >= lo && j < lo + len) z[j - lo] = INFINITY;
+    }
+    __syncthreads();
+    trace(1, 9);
+    int base_def = 0;
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
+    const int nt = need;
+    // ---- emit this slice ascending (a3 output): position = #definite before + #taken before
     for (int rd = 0; rd < rounds; ++rd) {
       const int j = rd * NT + tid;
-      bool f = false;
-      if (j < len) { const float zz = z[j]; f = (zz == INFINITY) || (zz > -INFINITY && zbucket(zz, zmax) < B); }
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (lane == 0) wcnt[rd * NW + warp] = __popc(bal);
-    }
-    __syncthreads();
-    {
-      int tot;                                           // rounds * NW <= NT (n_per <= 16384)
-      const int mine = tid < rounds * NW ? wcnt[tid] : 0;
-      const int ex = block_exclusive_scan<NT>(mine, tk, &tot);
-      if (tid < rounds * NW) wcnt[tid] = base + ex;
-    }
-    __syncthreads();
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int j = rd * NT + tid;
-      bool f = false;
-      if (j < len) { const float zz = z[j]; f = (zz == INFINITY) || (zz > -INFINITY && zbucket(zz, zmax) < B); }
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (f) {
-        const int pos = wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u));
-        out[pos] = lo + j;
-        if (sel_user) sel_user[bh * k + pos] = lo + j;
+      bool def = false, taken = false;
+      if (j < len) {
+        const float zz = z[j];
+        taken = zz == INFINITY;
+        def = !taken && zz > -INFINITY && zbucket(zz, zmax) < B;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, def);
+      if (def || taken) {
+        const int jj = lo + j;
+        int lo2 = 0;                                    // #taken with index < jj
+        if (nt <= 32) {
+#pragma unroll 8
+          for (int c = 0; c < nt; ++c) lo2 += tks[c] < jj;
+        } else {
+          int hi2 = nt;
+          while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < jj) lo2 = mid + 1; else hi2 = mid; }
+        }
+        const int pos = base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u)) + lo2;
+        out[pos] = jj;
+        if (sel_user) sel_user[bh * k + pos] = jj;
       }
     }
+    trace(1, 12);
     cluster_sync_all();                                                 // #3 DSMEM reads finished
   } else {                   // pathological score distribution: exact radix select on one CTA
     float* zg = zws + bh * n;
@@ -426,6 +466,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
   }
   trace(1, 7);
+  if (!early_trigger) pdl_trigger();
 }
 
 // =============================================================================================
@@ -497,18 +538,19 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
     const int nch = min(8, D.k - ui * 8);
     ntok = nch * kChunk;
     if (tid < kUnitTok) tok[tid] = tid < ntok ? sel[(size_t)bh * D.k + ui * 8 + (tid >> 3)] * kChunk + (tid & 7) : 0;
-    if (tid == 0) {
-      const int32_t* ids = sel + (size_t)bh * D.k + ui * 8;
-      // a4 operands first (HBM, needed first): 8 contiguous factor rows per chunk (2.5 KB at r = 160)
-      const uint32_t rb = kChunk * D.r * 2;
+    const uint32_t rb = kChunk * D.r * 2;
+    if (tid == 0) {                                      // arm both barriers before any copy is issued
       mbar_expect_tx(&barAB, nch * rb);
-      for (int c = 0; c < nch; ++c)
-        bulk_g2s(As + c * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)ids[c] * kChunk) * D.r, rb, &barAB);
-      // a5: value chunks straight from pinned host memory over PCIe (zero-copy bulk copies)
       mbar_expect_tx(&barV, nch * kChunk * kHeadDim * 2);
-      for (int c = 0; c < nch; ++c)
-        bulk_g2s(Vs + c * kChunk * kHeadDim,
-                 Ly.V_host + ((size_t)bh * D.s + (size_t)ids[c] * kChunk) * kHeadDim, kChunk * kHeadDim * 2, &barV);
+    }
+    __syncwarp();
+    if (tid < nch) {                                     // one issuing thread per chunk
+      const int id = sel[(size_t)bh * D.k + ui * 8 + tid];
+      // a4 operands first (HBM, needed first): 8 contiguous factor rows (2.5 KB at r = 160)
+      bulk_g2s(As + tid * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)id * kChunk) * D.r, rb, &barAB);
+      // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy)
+      bulk_g2s(Vs + tid * kChunk * kHeadDim, Ly.V_host + ((size_t)bh * D.s + (size_t)id * kChunk) * kHeadDim,
+               kChunk * kHeadDim * 2, &barV);
     }
     trace(2, 2);
     __syncthreads();
@@ -762,7 +804,7 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
   const int n_split = n_sel_u + n_out_u + n_win_max;
   const size_t BHq = (size_t)D.b * D.hq, BHk = (size_t)D.b * D.hk;
   char* p_log = carve(BHq * D.n_c * 4);
-  char* p_part = carve(BHq * tph * 4 * 8);          // per-(tile, quadrant) score partials
+  char* p_part = carve(BHq * kSegMax * 8);          // per-(score CTA, head) softmax partials
   char* p_z = carve(BHk * D.n_c * 4);                // select fallback / large-n_c slices
   char* p_sel = carve(BHk * D.k * 4);
   char* p_op = carve(BHq * n_split * kHeadDim * 4);
@@ -835,8 +877,10 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     if (nsp > 32 * kMergeMaxPerLane || (size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 > (size_t)(lay.q - lay.a))
       return cudaErrorInvalidConfiguration;                                           // merge scratch
   }
-  const int grid_s = total_tiles < 2 * num_sms() ? total_tiles : 2 * num_sms();
+  int grid_s = total_tiles < 2 * num_sms() ? total_tiles : 2 * num_sms();
+  while (grid_s > 1 && (long long)tph * grid_s / total_tiles + 2 > kSegMax) --grid_s;   // select's slots
   // a1: tcgen05 score (TMA + TMEM); CUDA-core fallback when tensor maps are unavailable
+  int score_grid = score_tc_grid(D, tph, num_sms());
   const char* nt = getenv("SKV_NO_TC");                 // test hook: force the CUDA-core score
   e = (nt && nt[0] == '1') ? cudaErrorNotSupported
                            : launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
@@ -844,6 +888,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (prof && e == cudaSuccess) profile_mark(prof, kScore, false, st);
   if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
     cudaGetLastError();
+    score_grid = grid_s;
     if (prof) profile_mark(prof, kScore, false, st);
     k_score<G><<<grid_s, 256, score_smem, st>>>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
                                                 v_new, Ly.K_win, Ly.V_win, step);
@@ -852,12 +897,16 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (e) return e;
   if (prof) { profile_mark(prof, kScore, true, st); profile_mark(prof, kSelect, false, st); }
   {
+    const char* et = getenv("SKV_EARLY_TRIGGER");         // tuning hook: 1 = PDL trigger at kernel start
+    const int early_sel = (et && et[0] == '1') ? 1 : 0;
     const bool zsm = z_fits_smem(D, G);
     const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
     if (zsm) e = launch_pdl(k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
-                            (const float*)ws.logits, (const float2*)ws.part, tph * 4, ws.z, ws.sel, sel_ids);
+                            (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
+                            ws.sel, sel_ids, early_sel);
     else e = launch_pdl(k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
-                        (const float*)ws.logits, (const float2*)ws.part, tph * 4, ws.z, ws.sel, sel_ids);
+                        (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
+                        ws.sel, sel_ids, early_sel);
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
   }

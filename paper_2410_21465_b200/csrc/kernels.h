@@ -33,7 +33,7 @@ struct BuildWs {
 struct DecodeWs {
   int* counters;     // [b][hk] zero-initialised by the caller once; every call leaves them zero
   float* logits;     // [b][hq][n_c]
-  float2* part;      // [b][hq][n_part]  per-(tile, quadrant) softmax partials (max, sumexp)
+  float2* part;      // [b][hq][kSegMax] per-(score CTA, head) softmax partials (max, sumexp)
   float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
   int32_t* sel;      // [b][hk][k]
   float* o_part;     // [b][hq][n_split][d]
@@ -48,6 +48,18 @@ constexpr size_t kSelectSmemMax = 160 * 1024;     // per-CTA z slice + its logit
 constexpr int kSelCL = 8;                         // select: CTAs per (request, KV head) cluster
 constexpr int kSelThreads = 512;
 constexpr int kSelCandLocal = 1024;               // threshold-bucket candidates per CTA
+constexpr int kSegMax = 64;                       // score partial slots per (b, q head)
+
+// first score CTA whose contiguous tile range [floor(c*T/g), floor((c+1)*T/g)) covers head bh
+// (32-bit: the host keeps total * grid < 2^31; 64-bit division is a slow software routine on the GPU)
+__host__ __device__ inline int seg_first(int bh, int tiles_per_head, int total, int grid) {
+  return (int)(((unsigned)(bh * tiles_per_head) * (unsigned)grid + (unsigned)grid - 1u) / (unsigned)total);
+}
+__host__ __device__ inline int seg_count(int bh, int tiles_per_head, int total, int grid) {
+  const unsigned last_tile = (unsigned)((bh + 1) * tiles_per_head - 1);
+  return (int)((last_tile * (unsigned)grid + (unsigned)grid - 1u) / (unsigned)total) -
+         seg_first(bh, tiles_per_head, total, grid) + 1;
+}
 
 inline size_t ws_header_bytes(const Dims& D) { return ((size_t)D.b * D.hk * 4 + 255) & ~(size_t)255; }
 size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base);
@@ -62,6 +74,7 @@ cudaError_t set_trace_buffer(void* dev_ptr);      // decode.cu: nullptr disables
 cudaError_t set_trace_buffer_tc(void* dev_ptr);   // score_tc.cu (kernel slot 0)
 
 // score_tc.cu: tcgen05 landmark scoring (a1); cudaErrorNotSupported if tensor maps are unavailable
+int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm);
 template <int G>
 cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
                             float* logits, float2* part, int tiles_per_head, float scale,

@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -85,10 +86,10 @@ __device__ __forceinline__ bool in_sorted(const int32_t* ids, int o, int j) {
 
 __device__ uint64_t* g_trace_tc = nullptr;              // same layout as decode.cu's trace buffer
 __device__ __forceinline__ void trace_tc(uint64_t* t, int ev) {
-  if (t != nullptr && threadIdx.x == 0) t[(size_t)blockIdx.x * 8 + ev] = globaltimer();
+  if (t != nullptr && threadIdx.x == 0) t[(size_t)blockIdx.x * 16 + ev] = globaltimer();
 }
 __device__ __forceinline__ void trace_tc_any(uint64_t* t, int ev) {   // caller restricts to one thread
-  if (t != nullptr) t[(size_t)blockIdx.x * 8 + ev] = globaltimer();
+  if (t != nullptr) t[(size_t)blockIdx.x * 16 + ev] = globaltimer();
 }
 
 }  // namespace
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __restrict__ oids,
            const uint16_t* __restrict__ q, float* __restrict__ logits, float2* __restrict__ part,
            int tiles_per_head, float scale, const uint16_t* __restrict__ k_new,
-           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step) {
+           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step, int early_trigger) {
   static_assert(G <= 16, "N = 16 covers the GQA group");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -110,6 +111,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], acc_full[kTcAcc], acc_empty[kTcAcc];
   __shared__ uint32_t tmem_base;
   __shared__ uint32_t obits[kTcMaxTiles * (kSTile / 32)];
+  __shared__ float2 wpart[4][16];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = D.b * D.hk * tiles_per_head;
   const int t_begin = (int)((long long)blockIdx.x * total / gridDim.x);
@@ -118,7 +120,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   const int bh0 = t_begin / tiles_per_head;
   uint64_t* const trace_buf = g_trace_tc;
   trace_tc(trace_buf, 0);
-  pdl_trigger();
+  if (early_trigger) pdl_trigger();
   // the producer thread initialises the barriers and puts the first kTcStages tiles in flight
   // before anything else, so HBM streaming starts at kernel entry
   if (tid == 4 * 32 && ntile > 0) {
@@ -126,6 +128,13 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     for (int s = 0; s < kTcAcc; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  if (warp == 0 && ntile > 0) {                        // TMEM: 8 accumulator buffers x 16 fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" :: "r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  pdl_wait();                                          // everything below may read the caller's inputs
+  if (tid == 4 * 32 && ntile > 0) {
     for (int i = 0; i < ntile && i < kTcStages; ++i) {
       const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
       const int row0 = bh * D.n_c + tile * kSTile;
@@ -135,10 +144,6 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     }
   }
   if (ntile <= 0) return;
-  if (warp == 0) {                                     // TMEM: 2 buffers x 4 chains x 16 fp32 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" :: "r"(smem_u32(&tmem_base)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
   const int nheads = (t_end - 1) / tiles_per_head - bh0 + 1;          // <= kTcMaxHeads (host check)
   // setup with every global load issued before any dependent use:
   //   B operands (q of each KV head in range, K-major SWIZZLE_128B, rows n >= G zero),
@@ -228,28 +233,37 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     }
   } else {
     // ---------------- epilogue: warps 0-3, TMEM lanes 32w .. 32w+31 ----------------
-    // per-thread online softmax partials over the CTA's rows of each KV head; one warp reduction
-    // per head segment (slot = first tile of the segment; the segment's other slots are emptied)
-    const int nq = tiles_per_head * 4;                    // partial slots per (b, q head)
+    // per-thread online softmax partials over the CTA's rows of each KV head, merged across the 4
+    // epilogue warps once per head segment: one partial per (CTA, KV head) at slot = CTA index minus
+    // the first CTA that covers the head (seg_first(); k_select recomputes the same mapping)
     float m_run[G], s_run[G];
 #pragma unroll
     for (int hq = 0; hq < G; ++hq) { m_run[hq] = -INFINITY; s_run[hq] = 0.f; }
-    int cur_bh = t_begin / tiles_per_head, first_tile = t_begin - cur_bh * tiles_per_head;
-    auto flush = [&](int bh, int slot_tile) {
+    int cur_bh = t_begin / tiles_per_head;
+    auto flush = [&](int bh) {
       const int b = bh / D.hk, h = bh - b * D.hk;
+      const int slot = (int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x);
 #pragma unroll
       for (int hq = 0; hq < G; ++hq) {
         const float m = warp_max(m_run[hq]);
         const float sc = (m > -INFINITY && m_run[hq] > -INFINITY) ? s_run[hq] * expf(m_run[hq] - m) : 0.f;
         const float sm = warp_sum(sc);
-        if (lane == hq) part[((size_t)b * D.hq + (size_t)h * G + hq) * nq + slot_tile * 4 + warp] = make_float2(m, sm);
+        if (lane == 0) wpart[warp][hq] = make_float2(m, sm);
         m_run[hq] = -INFINITY; s_run[hq] = 0.f;
       }
+      asm volatile("bar.sync 1, 128;" ::: "memory");     // the 4 epilogue warps
+      if (warp == 0 && lane < G) {
+        float m = -INFINITY, sm = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) lse_merge(m, sm, wpart[w][lane].x, wpart[w][lane].y);
+        part[((size_t)b * D.hq + (size_t)h * G + lane) * kSegMax + slot] = make_float2(m, sm);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
     };
     for (int i = 0; i < ntile; ++i) {
       const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
       const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
-      if (bh != cur_bh) { flush(cur_bh, first_tile); cur_bh = bh; first_tile = tile; }
+      if (bh != cur_bh) { flush(cur_bh); cur_bh = bh; }
       const int b = bh / D.hk, h = bh - b * D.hk;
       mbar_wait(&acc_full[buf], aph);
       tc_fence_after();
@@ -270,13 +284,12 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
           else if (x > -INFINITY) s_run[hq] += expf(x - m_run[hq]);
         }
       }
-      if (tile != first_tile && lane < G)
-        part[((size_t)b * D.hq + (size_t)h * G + lane) * nq + tile * 4 + warp] = make_float2(-INFINITY, 0.f);
     }
-    flush(cur_bh, first_tile);
+    flush(cur_bh);
   }
   __syncthreads();
   trace_tc(trace_buf, 1);
+  if (!early_trigger) pdl_trigger();
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" :: "r"(tmem));
@@ -310,6 +323,8 @@ int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm) {
   while (grid < total && ((total + grid - 1) / grid > (kTcMaxHeads - 1) * tiles_per_head ||
                           (total + grid - 1) / grid > kTcMaxTiles))
     grid = grid * 2 < total ? grid * 2 : total;
+  // at most kSegMax score CTAs may cover one KV head (k_select's partial slots)
+  while (grid > 1 && (long long)tiles_per_head * grid / total + 2 > kSegMax) --grid;
   return grid;
 }
 
@@ -337,9 +352,17 @@ cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oid
     attr = true;
   }
   const int grid = score_tc_grid(D, tiles_per_head, n_sm);
-  k_score_tc<G><<<grid, kTcThreads, score_tc_smem_bytes(), st>>>(map, D, oids, q, logits, part, tiles_per_head,
-                                                                scale, k_new, v_new, K_win, V_win, step);
-  return cudaGetLastError();
+  const char* et = getenv("SKV_EARLY_TRIGGER");            // tuning hook: 1 = PDL trigger at kernel start
+  const int early = (et && et[0] == '1') ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(kTcThreads); cfg.dynamicSmemBytes = score_tc_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;     // prologue overlaps the prior kernel
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_score_tc<G>, map, D, oids, q, logits, part, tiles_per_head, scale, k_new, v_new,
+                            K_win, V_win, step, early);
 }
 
 #define SKV_INST(G)                                                                                       \

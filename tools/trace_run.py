@@ -30,7 +30,7 @@ for l in range(args.layers):
     st.build(rope.struct, ws)
     states.append(st)
 out = torch.empty(cfg.batch, cfg.n_q_heads, 128, dtype=torch.bfloat16, device="cuda")
-tr = torch.zeros(4 * 4096 * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(4 * 4096 * 16, dtype=torch.int64, device="cuda")
 for step in range(6):
     for l, st in enumerate(states):
         si = synth.gen_step(cfg, 99, l, step, device="cuda")
@@ -42,9 +42,9 @@ for step in range(6):
         if step == 5 and l == args.layers - 1:
             torch.cuda.synchronize()
             bd.shadowkv_trace_buffer(None)
-t = tr.view(4, 4096, 8).cpu().numpy().astype(np.float64)
+t = tr.view(4, 4096, 16).cpu().numpy().astype(np.float64)
 t0 = t[0][t[0][:, 0] > 0][:, 0].min()
-names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand", "sync2", "end"],
+names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "-", "-", "emitted", "nseg", "loaded_max", "exp_sum"],
          3: ["merge_start", "weights"],
          2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end"]}
 for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
