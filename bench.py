@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="extra untimed pass timing every kernel")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: every rank runs the config's batch; strong: the batch is split over ranks")
+    ap.add_argument("--layer-states", type=int, default=0,
+                    help="distinct layer states cycled per step (default: the model's layer count)")
     return ap.parse_args()
 
 
@@ -63,7 +67,7 @@ def workload_config(cfg: synth.Config, n_gpus: int) -> dict:
             "n_q_heads": cfg.n_q_heads, "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
             "ctx_len": cfg.ctx_len, "layers": cfg.n_layers, "batch_per_gpu": cfg.batch,
             "global_batch": cfg.batch * n_gpus, "parallelism": f"requests sharded over {n_gpus} GPU(s), no collective",
-            "l2": "inputs > L2: 32 distinct layer states cycled every step (~2.5 GB HBM + 8.6 GB pinned host per GPU)",
+            "l2": "inputs > L2: `layer_states` distinct layer states (c2: 32 = ~2.5 GB HBM + 8.6 GB pinned host) cycled every step",
             "values": "offloaded to pinned host DRAM, gathered zero-copy over PCIe each step"}
 
 
@@ -244,10 +248,16 @@ def run_ours(args, cfg):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace, binding as bd
+    from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace, binding as bd, shard
 
     dev = "cuda"
+    if args.scaling == "strong":
+        pl = shard.plan(cfg.batch, cfg.n_q_heads, cfg.n_kv_heads, rank, world)
+        if pl.mode != "request":
+            raise SystemExit("strong scaling needs batch >= n_gpus")
+        cfg = cfg.replace(batch=pl.batch)
     Lm, b = cfg.n_layers, cfg.batch
+    n_states = args.layer_states or Lm
     n_total = args.warmup + 2 * args.steps + args.e2e_steps + 48
     shape = Shape.from_config(cfg, steps=n_total + 1)
     inv, rot, il = synth.rope_table(cfg)
@@ -257,10 +267,18 @@ def run_ours(args, cfg):
 
     # --- states: 32 distinct layers, values in one pinned+mapped host pool -------------------
     per_layer = b * cfg.n_kv_heads * cfg.ctx_len * cfg.head_dim
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+        if per_layer * 2 * n_states > 0.8 * avail:
+            raise SystemExit(f"{per_layer * 2 * n_states / 1e9:.1f} GB of pinned values exceed host RAM; "
+                             f"use --layer-states")
+    except ImportError:
+        pass
     t_setup = time.perf_counter()
-    pool = pinned_pool(per_layer * 2 * Lm)
+    pool = pinned_pool(per_layer * 2 * n_states)
     states = []
-    for l in range(Lm):
+    for l in range(n_states):
         inp = synth.gen_layer(cfg, seed, layer=l, device=dev)
         vh = pool[l * per_layer:(l + 1) * per_layer].view(b, cfg.n_kv_heads, cfg.ctx_len, cfg.head_dim)
         st = LayerState(shape, device=dev, V_host=vh)
@@ -286,7 +304,7 @@ def run_ours(args, cfg):
 
     def step(i, q, kn, vn):
         for l in range(Lm):
-            states[l].decode(rope.struct, q[l], kn[l], vn[l], i, out[l], ws, stream=stream)
+            states[l % n_states].decode(rope.struct, q[l], kn[l], vn[l], i, out[l], ws, stream=stream)
             launches[0] += bd.shadowkv_last_launch_count()
 
     for i in range(args.warmup):
@@ -304,12 +322,9 @@ def run_ours(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize()
     gpu_launches = launches[0]
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    value = b * world / (ms / 1e3)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    value = shard.job_tokens_per_s(b, ms_local / 1e3, device=dev)        # sum tokens / max time
+    ms = shard.max_over_ranks(ms_local, device=dev)
 
     # --- dominant-kernel timing: a second timed pass of K steps with CUDA events recorded on the
     #     launch stream around the fused sparse-attention kernel of every layer (kept out of the
@@ -345,11 +360,9 @@ def run_ours(args, cfg):
         stream.synchronize()                                   # host reads the step's result
     f1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / max(1, args.e2e_steps)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_local = f0.elapsed_time(f1) / max(1, args.e2e_steps)
+    e2e_value = shard.job_tokens_per_s(b, e2e_local / 1e3, device=dev)
+    e2e_ms = shard.max_over_ranks(e2e_local, device=dev)
 
     # --- roofline of the dominant kernel (fused rebuild+gather+attention: host-link bound) -----
     g_ms, g_cnt = prof["sparse_attn"]
@@ -379,11 +392,11 @@ def run_ours(args, cfg):
     hbm_peak, hbm_src = load_peaks()
     n_c = shape.n_c
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/; random rank-160 factors)",
-            "config": workload_config(cfg, world),
+            "config": dict(workload_config(cfg, world), layer_states=n_states),
             "roofline": roofline,
-            "e2e": {"value": b * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),

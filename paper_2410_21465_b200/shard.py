@@ -1,0 +1,83 @@
+"""Multi-GPU plumbing for the decode path (host logic only; no data-path collective).
+
+ShadowKV's per-layer decode step is independent per request and per KV head (Alg 2, P:160-185:
+every tensor is indexed by b and h_kv; the only cross-head object is the shared A of a request).
+So the path shards with no exchange step:
+
+  * by request: rank r owns requests [r*B/N, (r+1)*B/N)   (c3: 64 requests over N GPUs)
+  * by KV head when the batch is smaller than the world: rank r owns KV heads [r*H/N, (r+1)*H/N)
+    of every request (A replicated; its q heads follow the GQA map hq -> floor(hq/g), R2)
+
+torch.distributed (NCCL on GPUs, gloo in the CPU tests) is used only for the start barrier, the
+max-over-ranks step time and the token count; never on the data path.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced split of n units: rank gets [lo, hi)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    return n * rank // world, n * (rank + 1) // world
+
+
+@dataclasses.dataclass(frozen=True)
+class Plan:
+    mode: str              # "request" or "kv_head"
+    requests: tuple        # (lo, hi) request range owned by this rank
+    kv_heads: tuple        # (lo, hi) KV-head range owned by this rank
+    q_heads: tuple         # (lo, hi) query-head range (GQA map)
+
+    @property
+    def batch(self) -> int:
+        return self.requests[1] - self.requests[0]
+
+    @property
+    def n_kv_heads(self) -> int:
+        return self.kv_heads[1] - self.kv_heads[0]
+
+    @property
+    def n_q_heads(self) -> int:
+        return self.q_heads[1] - self.q_heads[0]
+
+
+def plan(batch: int, n_q_heads: int, n_kv_heads: int, rank: int, world: int) -> Plan:
+    """Request sharding when batch >= world, else KV-head sharding (every rank gets >= 1 unit)."""
+    g = n_q_heads // n_kv_heads
+    if batch >= world:
+        r = shard_range(batch, rank, world)
+        return Plan("request", r, (0, n_kv_heads), (0, n_q_heads))
+    if batch * n_kv_heads < world:
+        raise ValueError(f"{batch} requests x {n_kv_heads} KV heads cannot feed {world} ranks")
+    if batch != 1:
+        raise ValueError("KV-head sharding is defined for a single request (batch < world => batch 1 here)")
+    h = shard_range(n_kv_heads, rank, world)
+    return Plan("kv_head", (0, 1), h, (h[0] * g, h[1] * g))
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """Step time of the whole job = the slowest rank (timing rule)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, device=None) -> float:
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def job_tokens_per_s(tokens_this_rank: float, step_s_this_rank: float, device=None) -> float:
+    """Whole-job decode tokens/s: all ranks' tokens per step / max-over-ranks step time."""
+    return sum_over_ranks(tokens_this_rank, device) / max_over_ranks(step_s_this_rank, device)
