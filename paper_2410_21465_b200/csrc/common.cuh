@@ -92,6 +92,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
                " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
 // global (device or host-mapped) -> shared, completion signalled on `bar` (bytes % 16 == 0)
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -125,6 +128,24 @@ __device__ __forceinline__ int ld_dsmem_i32(uint32_t a) {
 }
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t a) {
   float v; asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v;
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v; asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+// spin (with backoff) until flag[0] != 0, then return flag[1] (read with acquire semantics by one
+// thread and broadcast through shared memory, so no thread can see a stale L1 copy)
+__device__ __forceinline__ int cta_wait_flag(const int* flag) {
+  __shared__ int bcast;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    while (ld_acquire_gpu(flag) == 0) __nanosleep(64);
+    bcast = ld_acquire_gpu(flag + 1);
+  }
+  __syncthreads();
+  return bcast;
 }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;

@@ -242,7 +242,7 @@ template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 1)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
          int score_total, int score_grid, float* __restrict__ zws, int32_t* __restrict__ sel,
-         int32_t* __restrict__ sel_user, int early_trigger) {
+         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int early_trigger) {
   TRACE_INIT;
   constexpr int NT = kSelThreads, NW = NT / 32;
   extern __shared__ __align__(16) float zdyn[];
@@ -319,6 +319,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   trace(1, 3);
   cluster_sync_all();                                                   // #1 histograms published
   trace(1, 4);
+  if (!early_trigger) pdl_trigger();                    // sparse CTAs launch and wait on the flags below
   int hv[kSelCL];                                       // thread i < 256 owns bin i of every rank
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) hv[r] = tid < 256 ? ld_dsmem_i32(dsmem_addr(&hist[tid], r)) : 0;
@@ -378,6 +379,20 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     const int mine = tid < rounds * NW ? wcnt[tid] : 0;
     const int ex = block_exclusive_scan<NT>(mine, tk, &tot);
     if (tid < rounds * NW) wcnt[tid] = ex;
+    __syncthreads();
+    // publish this slice's definite selections (bucket < B, ascending) at the cluster prefix:
+    // the sparse-attention CTAs start fetching their values before the threshold bucket is ranked
+    int base_def = 0;
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int j = rd * NT + tid;
+      bool def = false;
+      if (j < len) { const float zz = z[j]; def = zz > -INFINITY && zbucket(zz, zmax) < B; }
+      const unsigned bal = __ballot_sync(0xffffffffu, def);
+      if (def) out[base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u))] = lo + j;
+    }
+    __threadfence();
   }
   trace(1, 5);
   cluster_sync_all();                                                   // #2 candidates published
@@ -388,6 +403,14 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); }
   fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal;
+  int* fl = flags + bh * 4;
+  if (!fallback && crank == 0 && tid == 0) {
+    int nd = 0;
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r) nd += below[r];
+    fl[1] = nd;
+    st_release_gpu(&fl[0], 1);                           // definite selections ready
+  }
   if (!fallback) {
     // all ranks' candidates -> local smem; the taken ones (rank < need, larger z first, ties -> lower
     // index, R12) form a sorted index list used to place every selection
@@ -421,33 +444,37 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
     __syncthreads();
     trace(1, 9);
-    int base_def = 0;
+    if (crank == 0) {                                    // threshold-bucket selections, ascending
+      for (int i = tid; i < need; i += NT) selrest[bh * k + i] = tks[i];
+      __syncthreads();
+      if (tid == 0) { __threadfence(); fl[3] = need; st_release_gpu(&fl[2], 1); }
+    }
+    if (sel_user) {          // a3 parity output: the full selection, ascending (R12)
+      int base_def = 0;
 #pragma unroll
-    for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
-    const int nt = need;
-    // ---- emit this slice ascending (a3 output): position = #definite before + #taken before
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int j = rd * NT + tid;
-      bool def = false, taken = false;
-      if (j < len) {
-        const float zz = z[j];
-        taken = zz == INFINITY;
-        def = !taken && zz > -INFINITY && zbucket(zz, zmax) < B;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, def);
-      if (def || taken) {
-        const int jj = lo + j;
-        int lo2 = 0;                                    // #taken with index < jj
-        if (nt <= 32) {
-#pragma unroll 8
-          for (int c = 0; c < nt; ++c) lo2 += tks[c] < jj;
-        } else {
-          int hi2 = nt;
-          while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < jj) lo2 = mid + 1; else hi2 = mid; }
+      for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
+      const int nt = need;
+      for (int rd = 0; rd < rounds; ++rd) {
+        const int j = rd * NT + tid;
+        bool def = false, taken = false;
+        if (j < len) {
+          const float zz = z[j];
+          taken = zz == INFINITY;
+          def = !taken && zz > -INFINITY && zbucket(zz, zmax) < B;
         }
-        const int pos = base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u)) + lo2;
-        out[pos] = jj;
-        if (sel_user) sel_user[bh * k + pos] = jj;
+        const unsigned bal = __ballot_sync(0xffffffffu, def);
+        if (def || taken) {
+          const int jj = lo + j;
+          int lo2 = 0;                                    // #taken with index < jj
+          if (nt <= 32) {
+#pragma unroll 8
+            for (int c = 0; c < nt; ++c) lo2 += tks[c] < jj;
+          } else {
+            int hi2 = nt;
+            while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < jj) lo2 = mid + 1; else hi2 = mid; }
+          }
+          sel_user[bh * k + base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u)) + lo2] = jj;
+        }
       }
     }
     trace(1, 12);
@@ -463,10 +490,15 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       __syncthreads();
       if (sel_user)
         for (int i = tid; i < k; i += NT) sel_user[bh * k + i] = out[i];
+      if (tid == 0) {
+        __threadfence();
+        fl[1] = k; fl[3] = 0;
+        st_release_gpu(&fl[2], 1);
+        st_release_gpu(&fl[0], 1);
+      }
     }
   }
   trace(1, 7);
-  if (!early_trigger) pdl_trigger();
 }
 
 // =============================================================================================
@@ -488,218 +520,16 @@ __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
   return s;
 }
 
+// The last unit of a (b, h) to finish merges all partials (log-sum-exp) into out, then leaves the
+// counter and flags zeroed for the next call.  A function (not a shared label) so that both exits
+// of k_sparse_attn reach the CTA barriers below through structured control flow.
 template <int G>
-__global__ void __launch_bounds__(256, 2)
-k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const int32_t* __restrict__ sel, int step,
-              float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
-              int n_split, float scale, uint16_t* __restrict__ dbg, int* __restrict__ counters,
-              uint16_t* __restrict__ out) {
+__device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int bh, int n_split,
+                                              int* __restrict__ counters, int* __restrict__ flags,
+                                              const float* __restrict__ o_part, const float2* __restrict__ ml_part,
+                                              uint8_t* scratch, uint16_t* __restrict__ out) {
   TRACE_INIT;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const AttnSmem lay = attn_smem_layout(D.r, G);
-  uint16_t* Vs = reinterpret_cast<uint16_t*>(smem + lay.v);
-  uint16_t* As = reinterpret_cast<uint16_t*>(smem + lay.a);     // A rows [64][r]  or K tile [64][128]
-  uint16_t* Bs = reinterpret_cast<uint16_t*>(smem + lay.bmat);  // [r][128]
-  float* qs = reinterpret_cast<float*>(smem + lay.q);           // [G][128]
-  float* P = reinterpret_cast<float*>(smem + lay.p);            // [G][64]
-  int* tok = reinterpret_cast<int*>(smem + lay.tok);
-  __shared__ __align__(8) uint64_t barAB, barV;
-  __shared__ float2 ml[G];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = lane >> 4, sub = lane & 15;
-  const int BH = D.b * D.hk;
-  const int T_out = D.o * kChunk, T_win = D.w_eff + step + 1;
-  int u = blockIdx.x, kind, bh, ui;
-  if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
-  else {
-    u -= BH * n_sel_u;
-    const int per = n_out_u + n_win_u;
-    bh = u / per; ui = u - bh * per;
-    if (ui < n_out_u) kind = 1; else { kind = 2; ui -= n_out_u; }
-  }
-  const int b = bh / D.hk, h = bh - b * D.hk;
-  const int split = kind == 0 ? ui : (kind == 1 ? n_sel_u + ui : n_sel_u + n_out_u + ui);
-  trace(2, 0);
-  if (tid == 0) { mbar_init(&barAB, 1); mbar_init(&barV, 1); fence_mbar_init(); }
-  // q is a call input: stage it before waiting on the producer kernels
-  for (int i = tid; i < G * kHeadDim; i += 256)
-    qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
-  __syncthreads();
-  int ntok;
-  const int tx = tid & 15, ty = tid >> 4;      // key-tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
-  float acc[4][8];
-  if (kind == 0) {
-    const size_t bbytes = (size_t)D.r * kHeadDim * 2;
-    if (tid == 0) {   // B_h does not depend on the selection: fetch it before the PDL wait
-      asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&barAB)), "r"((uint32_t)bbytes) : "memory");
-      bulk_g2s(Bs, Ly.B + (size_t)bh * D.r * kHeadDim, (uint32_t)bbytes, &barAB);
-    }
-    pdl_wait();
-    trace(2, 1);
-    const int nch = min(8, D.k - ui * 8);
-    ntok = nch * kChunk;
-    if (tid < kUnitTok) tok[tid] = tid < ntok ? sel[(size_t)bh * D.k + ui * 8 + (tid >> 3)] * kChunk + (tid & 7) : 0;
-    const uint32_t rb = kChunk * D.r * 2;
-    if (tid == 0) {                                      // arm both barriers before any copy is issued
-      mbar_expect_tx(&barAB, nch * rb);
-      mbar_expect_tx(&barV, nch * kChunk * kHeadDim * 2);
-    }
-    __syncwarp();
-    if (tid < nch) {                                     // one issuing thread per chunk
-      const int id = sel[(size_t)bh * D.k + ui * 8 + tid];
-      // a4 operands first (HBM, needed first): 8 contiguous factor rows (2.5 KB at r = 160)
-      bulk_g2s(As + tid * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)id * kChunk) * D.r, rb, &barAB);
-      // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy)
-      bulk_g2s(Vs + tid * kChunk * kHeadDim, Ly.V_host + ((size_t)bh * D.s + (size_t)id * kChunk) * kHeadDim,
-               kChunk * kHeadDim * 2, &barV);
-    }
-    trace(2, 2);
-    __syncthreads();
-    mbar_wait(&barAB, 0);
-    trace(2, 3);
-    // ---- K~ = A_rows . B_h (fp32)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
-    const int r = D.r;
-    for (int rho = 0; rho < r; rho += 2) {
-      float b0[8], b1[8];
-      unpack8(*reinterpret_cast<const uint4*>(Bs + rho * kHeadDim + tx * 8), b0);
-      unpack8(*reinterpret_cast<const uint4*>(Bs + (rho + 1) * kHeadDim + tx * 8), b1);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(As + (ty + 16 * i) * r + rho);
-        const float a0 = bf_lo(a2), a1 = bf_hi(a2);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[i][e] = fmaf(a1, b1[e], fmaf(a0, b0[e], acc[i][e]));
-      }
-    }
-    // ---- RoPE at the tokens' absolute positions (R15), in registers
-    const int halfrot = R.rot >> 1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int t = tok[ty + 16 * i];
-      if (R.interleaved) {
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const int d0 = tx * 8 + e;
-          if (d0 < R.rot) {
-            float sn, cs;
-            rope_sincos(t, R.inv_freq[d0 >> 1], &sn, &cs);
-            const float x0 = acc[i][e], x1 = acc[i][e + 1];
-            acc[i][e] = x0 * cs - x1 * sn;
-            acc[i][e + 1] = x1 * cs + x0 * sn;
-          }
-        }
-      } else {
-        const int sh = halfrot >> 3;                       // partner lane offset (halfrot % 8 == 0)
-        const bool lowh = tx * 8 < halfrot, inrot = tx * 8 < R.rot;
-        const int src = (lane & 16) | (lowh ? tx + sh : tx - sh) & 15;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float pv = __shfl_sync(0xffffffffu, acc[i][e], inrot ? src : lane);
-          if (inrot) {
-            const int pi = (lowh ? tx * 8 : tx * 8 - halfrot) + e;
-            float sn, cs;
-            rope_sincos(t, R.inv_freq[pi], &sn, &cs);
-            acc[i][e] = lowh ? acc[i][e] * cs - pv * sn : acc[i][e] * cs + pv * sn;
-          }
-        }
-      }
-    }
-    if (dbg) {                                             // a4 parity hook (bf16 of the fp32 keys)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = ty + 16 * i;
-        if (row < ntok) {
-          uint4 kb = make_uint4(pack_bf2(acc[i][0], acc[i][1]), pack_bf2(acc[i][2], acc[i][3]),
-                                pack_bf2(acc[i][4], acc[i][5]), pack_bf2(acc[i][6], acc[i][7]));
-          *reinterpret_cast<uint4*>(dbg + (((size_t)bh * D.k * kChunk) + ui * kUnitTok + row) * kHeadDim + tx * 8) = kb;
-        }
-      }
-    }
-  } else {
-    // ---- outlier (P:133) or window (R8, R18) unit: exact keys and values from HBM
-    pdl_wait();
-    const uint16_t *Ksrc, *Vsrc;
-    if (kind == 1) {
-      ntok = min(kUnitTok, T_out - ui * kUnitTok);
-      Ksrc = Ly.K_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
-      Vsrc = Ly.V_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
-    } else {
-      ntok = min(kUnitTok, T_win - ui * kUnitTok);
-      Ksrc = Ly.K_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
-      Vsrc = Ly.V_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
-    }
-    if (tid == 0) {
-      mbar_expect_tx(&barAB, ntok * kHeadDim * 2);
-      bulk_g2s(As, Ksrc, ntok * kHeadDim * 2, &barAB);
-      mbar_expect_tx(&barV, ntok * kHeadDim * 2);
-      bulk_g2s(Vs, Vsrc, ntok * kHeadDim * 2, &barV);
-    }
-    mbar_wait(&barAB, 0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = ty + 16 * i;
-      if (row < ntok) unpack8(*reinterpret_cast<const uint4*>(As + row * kHeadDim + tx * 8), acc[i]);
-      else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
-      }
-    }
-  }
-  // ---- logits q . k for G heads: 4 tokens x (<= 4 heads) per lane per pass, reduced over 16 lanes
-  {
-    constexpr int HC = G < 4 ? G : 4;
-#pragma unroll
-    for (int h0 = 0; h0 < G; h0 += HC) {
-      float pv[16];
-#pragma unroll
-      for (int x = 0; x < 16; ++x) pv[x] = 0.f;
-#pragma unroll
-      for (int hh = 0; hh < HC; ++hh) {
-        const float4* qp = reinterpret_cast<const float4*>(qs + (h0 + hh) * kHeadDim + tx * 8);
-        const float4 q0 = qp[0], q1 = qp[1];
-        const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float a = 0.f;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) a = fmaf(qv[e], acc[i][e], a);
-          pv[i * HC + hh] = a;
-        }
-      }
-      reduce_scatter16<16>(pv, sub);
-      if (sub < 4 * HC) {
-        const int i = sub / HC, hq = h0 + sub % HC, row = ty + 16 * i;
-        P[hq * kUnitTok + row] = row < ntok ? pv[0] * scale : -INFINITY;
-      }
-    }
-  }
-  __syncthreads();
-  // ---- softmax statistics of this unit (per q head)
-  for (int hq = warp; hq < G; hq += 8) {
-    float x0 = P[hq * kUnitTok + lane], x1 = P[hq * kUnitTok + lane + 32];
-    const float m = warp_max(fmaxf(x0, x1));
-    const float e0 = expf(x0 - m), e1 = expf(x1 - m);
-    P[hq * kUnitTok + lane] = e0;
-    P[hq * kUnitTok + lane + 32] = e1;
-    const float l = warp_sum(e0 + e1);
-    if (lane == 0) ml[hq] = make_float2(m, l);
-  }
-  trace(2, 4);
-  mbar_wait(&barV, 0);                                   // values (from PCIe for selected units)
-  trace(2, 5);
-  __syncthreads();
-  // ---- PV: thread = (dim, head parity)
-  const int d = tid & 127, hh = tid >> 7;
-  for (int hq = hh; hq < G; hq += 2) {
-    float a = 0.f;
-    for (int t = 0; t < ntok; ++t) a = fmaf(P[hq * kUnitTok + t], bf2f(Vs[t * kHeadDim + d]), a);
-    const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-    o_part[row * kHeadDim + d] = a;
-    if (d == 0) ml_part[row] = ml[hq];
-  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- the last unit of this (b, h) to finish merges all partials (log-sum-exp) -> out
   __shared__ int is_last;
   __syncthreads();                                     // all partial stores of this CTA issued
@@ -711,7 +541,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
   trace(2, 6);
   __syncthreads();
   if (!is_last) return;
-  float* wsm = reinterpret_cast<float*>(smem + lay.a);          // [G][n_split] weights (A/B region is free)
+  float* wsm = reinterpret_cast<float*>(scratch);          // [G][n_split] weights (A/B region is free)
   trace(3, 0);
   for (int hq = warp; hq < G; hq += 8) {
     const float2* mlr = ml_part + ((size_t)b * D.hq + (size_t)h * G + hq) * n_split;
@@ -784,7 +614,257 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
     __syncthreads();
   }
   trace(2, 7);
-  if (tid == 0) counters[bh] = 0;                      // leave the workspace counter zeroed
+  if (tid == 0) {                                      // leave counter and flags zeroed for the next call
+    counters[bh] = 0;
+    int* fl2 = flags + (size_t)bh * 4;
+    fl2[0] = 0; fl2[1] = 0; fl2[2] = 0; fl2[3] = 0;
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256, 2)
+k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const int32_t* __restrict__ seldef,
+              const int32_t* __restrict__ selrest, int* __restrict__ flags, int step,
+              float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
+              int n_split, float scale, uint16_t* __restrict__ dbg, int* __restrict__ counters,
+              uint16_t* __restrict__ out) {
+  TRACE_INIT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const AttnSmem lay = attn_smem_layout(D.r, G);
+  uint16_t* Vs = reinterpret_cast<uint16_t*>(smem + lay.v);
+  uint16_t* As = reinterpret_cast<uint16_t*>(smem + lay.a);     // A rows [64][r]  or K tile [64][128]
+  uint16_t* Bs = reinterpret_cast<uint16_t*>(smem + lay.bmat);  // [r][128]
+  float* qs = reinterpret_cast<float*>(smem + lay.q);           // [G][128]
+  float* P = reinterpret_cast<float*>(smem + lay.p);            // [G][64]
+  int* tok = reinterpret_cast<int*>(smem + lay.tok);
+  __shared__ __align__(8) uint64_t barAB, barV;
+  __shared__ float2 ml[G];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane & 15;
+  const int d = tid & 127, hh = tid >> 7;                      // PV / merge ownership: dim, head parity
+  const int BH = D.b * D.hk;
+  const int T_out = D.o * kChunk, T_win = D.w_eff + step + 1;
+  int u = blockIdx.x, kind, bh, ui;
+  if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
+  else {
+    u -= BH * n_sel_u;
+    const int per = n_out_u + n_win_u;
+    bh = u / per; ui = u - bh * per;
+    if (ui < n_out_u) kind = 1; else { kind = 2; ui -= n_out_u; }
+  }
+  const int b = bh / D.hk, h = bh - b * D.hk;
+  const int split = kind == 0 ? ui : (kind == 1 ? n_sel_u + ui : n_sel_u + n_out_u + ui);
+  trace(2, 0);
+  if (tid == 0) { mbar_init(&barAB, 1); mbar_init(&barV, 1); fence_mbar_init(); }
+  // q is a call input: stage it before waiting on the producer kernels
+  for (int i = tid; i < G * kHeadDim; i += 256)
+    qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
+  __syncthreads();
+  int ntok;
+  const int tx = tid & 15, ty = tid >> 4;      // key-tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
+  float acc[4][8];
+  if (kind == 0) {
+    const size_t bbytes = (size_t)D.r * kHeadDim * 2;
+    if (tid == 0) {   // B_h does not depend on the selection: fetch it before the PDL wait
+      asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&barAB)), "r"((uint32_t)bbytes) : "memory");
+      bulk_g2s(Bs, Ly.B + (size_t)bh * D.r * kHeadDim, (uint32_t)bbytes, &barAB);
+    }
+    // selection published by k_select in two parts: the definite chunks (above the threshold
+    // bucket) as soon as the histogram is known, then the ranked threshold-bucket chunks
+    int* fl = flags + (size_t)bh * 4;
+    const int n_def = cta_wait_flag(&fl[0]), nd_u = (n_def + 7) >> 3;
+    trace(2, 1);
+    const int32_t* list;
+    int nch;
+    if (ui < nd_u) { list = seldef + (size_t)bh * D.k + ui * 8; nch = min(8, n_def - ui * 8); }
+    else {
+      const int n_rest = cta_wait_flag(&fl[2]), u2 = ui - nd_u;
+      list = selrest + (size_t)bh * D.k + u2 * 8;
+      nch = max(0, min(8, n_rest - u2 * 8));
+    }
+    ntok = nch * kChunk;
+    if (ntok == 0) {                                     // spare unit slot: empty partial
+      for (int hq = tid >> 7; hq < G; hq += 2) {
+        const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+        o_part[row * kHeadDim + (tid & 127)] = 0.f;
+        if ((tid & 127) == 0) ml_part[row] = make_float2(-INFINITY, 0.f);
+      }
+      if (tid == 0) mbar_arrive_plain(&barAB);          // B_h was expected without an arrival
+      mbar_wait(&barAB, 0);                              // retire the B_h copy before leaving
+      sparse_finish<G>(D, b, h, bh, n_split, counters, flags, o_part, ml_part, smem + lay.a, out);
+      return;
+    }
+    if (tid < kUnitTok) tok[tid] = tid < ntok ? list[tid >> 3] * kChunk + (tid & 7) : 0;
+    const uint32_t rb = kChunk * D.r * 2;
+    if (tid == 0) {                                      // arm both barriers before any copy is issued
+      mbar_expect_tx(&barAB, nch * rb);
+      mbar_expect_tx(&barV, nch * kChunk * kHeadDim * 2);
+    }
+    __syncwarp();
+    if (tid < nch) {                                     // one issuing thread per chunk
+      const int id = list[tid];
+      // a4 operands first (HBM, needed first): 8 contiguous factor rows (2.5 KB at r = 160)
+      bulk_g2s(As + tid * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)id * kChunk) * D.r, rb, &barAB);
+      // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy)
+      bulk_g2s(Vs + tid * kChunk * kHeadDim, Ly.V_host + ((size_t)bh * D.s + (size_t)id * kChunk) * kHeadDim,
+               kChunk * kHeadDim * 2, &barV);
+    }
+    trace(2, 2);
+    __syncthreads();
+    mbar_wait(&barAB, 0);
+    trace(2, 3);
+    // ---- K~ = A_rows . B_h (fp32)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
+    const int r = D.r;
+    for (int rho = 0; rho < r; rho += 2) {
+      float b0[8], b1[8];
+      unpack8(*reinterpret_cast<const uint4*>(Bs + rho * kHeadDim + tx * 8), b0);
+      unpack8(*reinterpret_cast<const uint4*>(Bs + (rho + 1) * kHeadDim + tx * 8), b1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(As + (ty + 16 * i) * r + rho);
+        const float a0 = bf_lo(a2), a1 = bf_hi(a2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[i][e] = fmaf(a1, b1[e], fmaf(a0, b0[e], acc[i][e]));
+      }
+    }
+    // ---- RoPE at the tokens' absolute positions (R15), in registers
+    const int halfrot = R.rot >> 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int t = tok[ty + 16 * i];
+      if (R.interleaved) {
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const int d0 = tx * 8 + e;
+          if (d0 < R.rot) {
+            float sn, cs;
+            rope_sincos(t, R.inv_freq[d0 >> 1], &sn, &cs);
+            const float x0 = acc[i][e], x1 = acc[i][e + 1];
+            acc[i][e] = x0 * cs - x1 * sn;
+            acc[i][e + 1] = x1 * cs + x0 * sn;
+          }
+        }
+      } else {
+        const int sh = halfrot >> 3;                       // partner lane offset (halfrot % 8 == 0)
+        const bool lowh = tx * 8 < halfrot, inrot = tx * 8 < R.rot;
+        const int src = (lane & 16) | (lowh ? tx + sh : tx - sh) & 15;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float pv = __shfl_sync(0xffffffffu, acc[i][e], inrot ? src : lane);
+          if (inrot) {
+            const int pi = (lowh ? tx * 8 : tx * 8 - halfrot) + e;
+            float sn, cs;
+            rope_sincos(t, R.inv_freq[pi], &sn, &cs);
+            acc[i][e] = lowh ? acc[i][e] * cs - pv * sn : acc[i][e] * cs + pv * sn;
+          }
+        }
+      }
+    }
+    if (dbg) {                        // a4 parity hook: bf16 of the fp32 keys at the chunk's rank in
+      const int n_rest = cta_wait_flag(&fl[2]);   // the ascending selection (= #definite + #rest below)
+      const int32_t* dl = seldef + (size_t)bh * D.k;
+      const int32_t* rl = selrest + (size_t)bh * D.k;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = ty + 16 * i;
+        if (row < ntok) {
+          const int cid = tok[row] >> 3;
+          int lo2 = 0, hi2 = n_def;
+          while (lo2 < hi2) { const int m = (lo2 + hi2) >> 1; if (dl[m] < cid) lo2 = m + 1; else hi2 = m; }
+          int lo3 = 0, hi3 = n_rest;
+          while (lo3 < hi3) { const int m = (lo3 + hi3) >> 1; if (rl[m] < cid) lo3 = m + 1; else hi3 = m; }
+          const int pos = lo2 + lo3;
+          uint4 kb = make_uint4(pack_bf2(acc[i][0], acc[i][1]), pack_bf2(acc[i][2], acc[i][3]),
+                                pack_bf2(acc[i][4], acc[i][5]), pack_bf2(acc[i][6], acc[i][7]));
+          *reinterpret_cast<uint4*>(dbg + (((size_t)bh * D.k + pos) * kChunk + (row & 7)) * kHeadDim + tx * 8) = kb;
+        }
+      }
+    }
+  } else {
+    // ---- outlier (P:133) or window (R8, R18) unit: exact keys and values from HBM
+    cta_wait_flag(&flags[(size_t)bh * 4]);              // (score's window append is visible)
+    const uint16_t *Ksrc, *Vsrc;
+    if (kind == 1) {
+      ntok = min(kUnitTok, T_out - ui * kUnitTok);
+      Ksrc = Ly.K_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
+      Vsrc = Ly.V_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
+    } else {
+      ntok = min(kUnitTok, T_win - ui * kUnitTok);
+      Ksrc = Ly.K_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
+      Vsrc = Ly.V_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
+    }
+    if (tid == 0) {
+      mbar_expect_tx(&barAB, ntok * kHeadDim * 2);
+      bulk_g2s(As, Ksrc, ntok * kHeadDim * 2, &barAB);
+      mbar_expect_tx(&barV, ntok * kHeadDim * 2);
+      bulk_g2s(Vs, Vsrc, ntok * kHeadDim * 2, &barV);
+    }
+    mbar_wait(&barAB, 0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = ty + 16 * i;
+      if (row < ntok) unpack8(*reinterpret_cast<const uint4*>(As + row * kHeadDim + tx * 8), acc[i]);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
+      }
+    }
+  }
+  // ---- logits q . k for G heads: 4 tokens x (<= 4 heads) per lane per pass, reduced over 16 lanes
+  {
+    constexpr int HC = G < 4 ? G : 4;
+#pragma unroll
+    for (int h0 = 0; h0 < G; h0 += HC) {
+      float pv[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) pv[x] = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < HC; ++hh) {
+        const float4* qp = reinterpret_cast<const float4*>(qs + (h0 + hh) * kHeadDim + tx * 8);
+        const float4 q0 = qp[0], q1 = qp[1];
+        const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float a = 0.f;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) a = fmaf(qv[e], acc[i][e], a);
+          pv[i * HC + hh] = a;
+        }
+      }
+      reduce_scatter16<16>(pv, sub);
+      if (sub < 4 * HC) {
+        const int i = sub / HC, hq = h0 + sub % HC, row = ty + 16 * i;
+        P[hq * kUnitTok + row] = row < ntok ? pv[0] * scale : -INFINITY;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- softmax statistics of this unit (per q head)
+  for (int hq = warp; hq < G; hq += 8) {
+    float x0 = P[hq * kUnitTok + lane], x1 = P[hq * kUnitTok + lane + 32];
+    const float m = warp_max(fmaxf(x0, x1));
+    const float e0 = expf(x0 - m), e1 = expf(x1 - m);
+    P[hq * kUnitTok + lane] = e0;
+    P[hq * kUnitTok + lane + 32] = e1;
+    const float l = warp_sum(e0 + e1);
+    if (lane == 0) ml[hq] = make_float2(m, l);
+  }
+  trace(2, 4);
+  mbar_wait(&barV, 0);                                   // values (from PCIe for selected units)
+  trace(2, 5);
+  __syncthreads();
+  // ---- PV: thread = (dim, head parity)
+  for (int hq = hh; hq < G; hq += 2) {
+    float a = 0.f;
+    for (int t = 0; t < ntok; ++t) a = fmaf(P[hq * kUnitTok + t], bf2f(Vs[t * kHeadDim + d]), a);
+    const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+    o_part[row * kHeadDim + d] = a;
+    if (d == 0) ml_part[row] = ml[hq];
+  }
+  sparse_finish<G>(D, b, h, bh, n_split, counters, flags, o_part, ml_part, smem + lay.a, out);
 }
 
 // =============================================================================================
@@ -799,14 +879,15 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
   size_t off = ws_header_bytes(D);                  // zero-initialised per-(b,h) counters live first
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return base + o; };
   const int tph = tiles_per_head(D);
-  const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+  const int n_sel_u = (D.k + 7) / 8 + 1, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
   const int n_win_max = (D.wcap + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_max;
   const size_t BHq = (size_t)D.b * D.hq, BHk = (size_t)D.b * D.hk;
   char* p_log = carve(BHq * D.n_c * 4);
   char* p_part = carve(BHq * kSegMax * 8);          // per-(score CTA, head) softmax partials
   char* p_z = carve(BHk * D.n_c * 4);                // select fallback / large-n_c slices
-  char* p_sel = carve(BHk * D.k * 4);
+  char* p_sel = carve(BHk * D.k * 4);                // definite selections (and the radix fallback)
+  char* p_rest = carve(BHk * D.k * 4);               // threshold-bucket selections
   char* p_op = carve(BHq * n_split * kHeadDim * 4);
   char* p_ml = carve(BHq * n_split * 8);
   if (ws) {
@@ -817,6 +898,8 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
     ws->o_part = reinterpret_cast<float*>(p_op);
     ws->ml_part = reinterpret_cast<float2*>(p_ml);
     ws->counters = reinterpret_cast<int*>(base);
+    ws->flags = reinterpret_cast<int*>(base) + (size_t)D.b * D.hk;
+    ws->selrest = reinterpret_cast<int32_t*>(p_rest);
     ws->n_sblk = tph;
     ws->n_split = n_split;
   }
@@ -872,7 +955,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   const int tph = ws.n_sblk;
   const int total_tiles = D.b * D.hk * tph;
   {
-    const int nsu = (D.k + 7) / 8, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+    const int nsu = (D.k + 7) / 8 + 1, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
     const int nsp = nsu + nou + (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
     if (nsp > 32 * kMergeMaxPerLane || (size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 > (size_t)(lay.q - lay.a))
       return cudaErrorInvalidConfiguration;                                           // merge scratch
@@ -903,20 +986,21 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
     if (zsm) e = launch_pdl(k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                             (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
-                            ws.sel, sel_ids, early_sel);
+                            ws.sel, ws.selrest, ws.flags, sel_ids, early_sel);
     else e = launch_pdl(k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                         (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
-                        ws.sel, sel_ids, early_sel);
+                        ws.sel, ws.selrest, ws.flags, sel_ids, early_sel);
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
   }
-  const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+  // definite + threshold-bucket chunks may straddle one extra 8-chunk unit
+  const int n_sel_u = (D.k + 7) / 8 + 1, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
   const int n_win_u = (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_u;
   const int units = D.b * D.hk * n_split;
   if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
-                      (const int32_t*)ws.sel, step, ws.o_part, ws.ml_part, n_sel_u, n_out_u, n_win_u, n_split, scale,
-                      dbg_keys, ws.counters, out))) return e;
+                      (const int32_t*)ws.sel, (const int32_t*)ws.selrest, ws.flags, step, ws.o_part, ws.ml_part,
+                      n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, ws.counters, out))) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
   *launches += 3;
   return cudaGetLastError();

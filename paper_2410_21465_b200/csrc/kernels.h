@@ -32,6 +32,8 @@ struct BuildWs {
 };
 struct DecodeWs {
   int* counters;     // [b][hk] zero-initialised by the caller once; every call leaves them zero
+  int* flags;        // [b][hk][4] {def_ready, n_def, rest_ready, n_rest}; zeroed again by each call's merger
+  int32_t* selrest;  // [b][hk][k] threshold-bucket selections, ascending
   float* logits;     // [b][hq][n_c]
   float2* part;      // [b][hq][kSegMax] per-(score CTA, head) softmax partials (max, sumexp)
   float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
@@ -61,7 +63,8 @@ __host__ __device__ inline int seg_count(int bh, int tiles_per_head, int total, 
          seg_first(bh, tiles_per_head, total, grid) + 1;
 }
 
-inline size_t ws_header_bytes(const Dims& D) { return ((size_t)D.b * D.hk * 4 + 255) & ~(size_t)255; }
+// header: per-(b,h) merge counter + 4 selection flags {def_ready, n_def, rest_ready, n_rest}
+inline size_t ws_header_bytes(const Dims& D) { return ((size_t)D.b * D.hk * 5 * 4 + 255) & ~(size_t)255; }
 size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base);
 size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base);
 
