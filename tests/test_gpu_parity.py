@@ -146,3 +146,48 @@ def test_decode_deterministic_and_unpinned_rejected():
     bad.V_host = torch.empty(P.shape.batch, C1.n_kv_heads, C1.ctx_len, 128, dtype=torch.bfloat16)  # pageable
     with pytest.raises(bd.ShadowKVError, match="SKV_ESTATE"):
         bad.build(P.rope.struct, P.ws)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_full_size_sampled(name):
+    """The other BASELINE configs at full size in the bench's launch configuration (whole per-GPU batch
+    in one call: c3 64 x 122K, c4 1M ctx with k = 2048, c5 GLM 12 x 256K with g = 16).  The oracle
+    cannot build the whole batch in seconds, so it builds + decodes sampled requests (first, last) from
+    the same generator inputs; the GPU state of those requests is then replaced by the oracle's bytes
+    so the decode comparison runs on identical state (as in test_decode_parity_identical_state)."""
+    from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
+    cfg = synth.CONFIGS[name]
+    shape = Shape.from_config(cfg, steps=2)
+    inp = synth.gen_layer(cfg, 7, device="cuda")                 # generator output, not the CUDA path's
+    st = LayerState(shape)
+    st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
+    inv, rot, il = synth.rope_table(cfg)
+    rope = RopeTable(inv, rot, il)
+    ws = alloc_workspace(shape)
+    st.build(rope.struct, ws)
+    torch.cuda.synchronize()
+    sample = sorted({0, cfg.batch - 1})
+    A64 = f64(inp["A"][sample]); B64 = f64(inp["B"][sample]); V64 = f64(inp["V"][sample].cpu())
+    del inp
+    ost = O.build(A64, B64, V64, inv, rot, il, cfg.chunk, cfg.n_outlier, cfg.window_ctx, shape.window_cap)
+    bf = torch.bfloat16
+    for j, bi in enumerate(sample):
+        assert_bf16_close(f64(st.landmarks[bi]), ost.landmarks[j], what=f"landmarks b={bi}")
+        gids = st.outlier_ids[bi].cpu().numpy()
+        for h in range(cfg.n_kv_heads):
+            assert outliers_valid(gids[h], ost.mincos[j, h], cfg.n_outlier)
+        st.landmarks[bi].copy_(torch.from_numpy(ost.landmarks[j]).to(bf))
+        st.outlier_ids[bi].copy_(torch.from_numpy(ost.outlier_ids[j]).to(torch.int32))
+        st.K_out[bi].copy_(torch.from_numpy(ost.K_out[j]).to(bf)); st.V_out[bi].copy_(torch.from_numpy(ost.V_out[j]).to(bf))
+        st.K_win[bi].copy_(torch.from_numpy(ost.K_win[j]).to(bf)); st.V_win[bi].copy_(torch.from_numpy(ost.V_win[j]).to(bf))
+    si = synth.gen_step(cfg, 7, 0, 0)
+    out = torch.empty(cfg.batch, cfg.n_q_heads, cfg.head_dim, dtype=bf, device="cuda")
+    sel = torch.empty(cfg.batch, cfg.n_kv_heads, cfg.budget, dtype=torch.int32, device="cuda")
+    dbg = torch.empty(cfg.batch, cfg.n_kv_heads, cfg.budget * cfg.chunk, cfg.head_dim, dtype=bf, device="cuda")
+    st.decode(rope.struct, si["q"].cuda(), si["k_new"].cuda(), si["v_new"].cuda(), 0, out, ws, sel_ids=sel, dbg_keys=dbg)
+    torch.cuda.synchronize()
+    oout, osel, oz, okeys, _ = O.decode_step(ost, A64, B64, V64, f64(si["q"][sample]), f64(si["k_new"][sample]),
+                                             f64(si["v_new"][sample]), 0, cfg.budget, inv, rot, il, cfg.chunk)
+    sub = cfg.replace(batch=len(sample))
+    check_decode(sub, f64(out[sample]), sel[sample].cpu().numpy(), f64(dbg[sample]), oout, osel, oz, okeys)
+    assert torch.isfinite(out.float()).all()                      # the unsampled requests ran too
