@@ -257,7 +257,6 @@ def run_ours(args, cfg):
             raise SystemExit("strong scaling needs batch >= n_gpus")
         cfg = cfg.replace(batch=pl.batch)
     Lm, b = cfg.n_layers, cfg.batch
-    n_states = args.layer_states or Lm
     n_total = args.warmup + 2 * args.steps + args.e2e_steps + 48
     shape = Shape.from_config(cfg, steps=n_total + 1)
     inv, rot, il = synth.rope_table(cfg)
@@ -265,16 +264,18 @@ def run_ours(args, cfg):
     ws = alloc_workspace(shape, device=dev)
     seed = args.seed + 7919 * rank
 
-    # --- states: 32 distinct layers, values in one pinned+mapped host pool -------------------
+    # --- states: L_m distinct layers (fewer if host RAM / HBM cannot hold them; every state is
+    #     far larger than L2 either way), values in one pinned+mapped host pool -------------------
     per_layer = b * cfg.n_kv_heads * cfg.ctx_len * cfg.head_dim
-    try:
-        import psutil
-        avail = psutil.virtual_memory().available
-        if per_layer * 2 * n_states > 0.8 * avail:
-            raise SystemExit(f"{per_layer * 2 * n_states / 1e9:.1f} GB of pinned values exceed host RAM; "
-                             f"use --layer-states")
-    except ImportError:
-        pass
+    dev_layer = 2 * b * (cfg.ctx_len * cfg.rank + cfg.n_kv_heads * (shape.n_c * cfg.head_dim + cfg.rank * cfg.head_dim
+                                                                     + 2 * (cfg.n_outlier * cfg.chunk + shape.window_cap) * cfg.head_dim))
+    import psutil
+    host_cap = int(0.6 * psutil.virtual_memory().available / world // (per_layer * 2))
+    dev_cap = int(0.7 * torch.cuda.mem_get_info()[0] // dev_layer)
+    n_states = args.layer_states or max(1, min(Lm, host_cap, dev_cap))
+    if per_layer * 2 * n_states > 0.8 * psutil.virtual_memory().available / world:
+        raise SystemExit(f"{per_layer * 2 * n_states / 1e9:.1f} GB of pinned values exceed host RAM; "
+                         f"use a smaller --layer-states")
     t_setup = time.perf_counter()
     pool = pinned_pool(per_layer * 2 * n_states)
     states = []
