@@ -135,6 +135,14 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
+// relaxed (coherent at gpu scope, unordered): for values that are their own payload, e.g. a
+// published chunk id that a consumer polls for
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v; asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
 // spin (with backoff) until flag[0] != 0, then return flag[1] (read with acquire semantics by one
 // thread and broadcast through shared memory, so no thread can see a stale L1 copy)
 __device__ __forceinline__ int cta_wait_flag(const int* flag) {

@@ -271,6 +271,8 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   if (tid == 0) { ccnt = 0; info[0] = info[1] = 0; }
   pdl_wait();
   trace(1, 1);
+  int* fl = flags + bh * 4;
+  if (crank == 0 && tid == 0) st_release_gpu(&fl[0], 1);  // score (incl. a7 window append) complete
   // ---- lse_hq from the score CTAs' per-segment partials: max-reduce, one exp per lane, sum-reduce
   //      (short dependent chains; fixed order, deterministic)
   if (warp < G) {
@@ -349,16 +351,17 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   }
   __syncthreads();
   const int B = info[0], need = info[1];
-  // per-rank count of elements strictly above the threshold bucket (the "definite" selections)
-#pragma unroll
-  for (int r = 0; r < kSelCL; ++r) {
-    const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
-    if (lane == 0) wtmp[warp * kSelCL + r] = v;
-  }
-  bool fallback = B == 255 || n_per > 16384;
-  const int rounds = (len + NT - 1) / NT;                             // <= 32 when n_per <= 16384
-  if (!fallback) {
-    // one pass: threshold-bucket candidates + per-(round, warp) counts of definite elements
+  // The selection is published UNORDERED into k slots (chunk id + 1; 0 = not yet): attention is a
+  // sum over the selected set, so no prefix scan has to run before a value fetch can start.  The
+  // chunks strictly above the threshold bucket ("definite") take slots [0, k - need) through one
+  // atomic reservation per warp right away; the `need` winners of the threshold bucket take
+  // [k - need, k) once ranked.  Each sparse-attention unit polls its own 8 slots.
+  int32_t* slots = sel + bh * k;
+  const int rounds = (len + NT - 1) / NT;
+  const bool prepub = !(B == 255 || n_per > 16384);       // else: radix fallback publishes all k
+  bool fallback = !prepub;
+  if (prepub) {
+    int wdef = 0;                                         // pass 1: candidates + definite count
     for (int rd = 0; rd < rounds; ++rd) {
       const int j = rd * NT + tid;
       int bk = 256;
@@ -368,52 +371,36 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
         const int pos = atomicAdd(&ccnt, 1);
         if (pos < kSelCandLocal) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, bk < B);
-      if (lane == 0) wcnt[rd * NW + warp] = __popc(bal);
+      const int c = __popc(__ballot_sync(0xffffffffu, bk < B));
+      if (lane == 0) wcnt[rd * NW + warp] = c;
+      wdef += c;
     }
-  }
-  __syncthreads();
-  if (tid < kSelCL) { int t = 0; for (int w = 0; w < NW; ++w) t += wtmp[w * kSelCL + tid]; below[tid] = t; }
-  if (!fallback) {                                      // exclusive scan of the definite counts
-    int tot;
-    const int mine = tid < rounds * NW ? wcnt[tid] : 0;
-    const int ex = block_exclusive_scan<NT>(mine, tk, &tot);
-    if (tid < rounds * NW) wcnt[tid] = ex;
-    __syncthreads();
-    // publish this slice's definite selections (bucket < B, ascending) at the cluster prefix:
-    // the sparse-attention CTAs start fetching their values before the threshold bucket is ranked
-    int base_def = 0;
-#pragma unroll
-    for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int j = rd * NT + tid;
-      bool def = false;
-      if (j < len) { const float zz = z[j]; def = zz > -INFINITY && zbucket(zz, zmax) < B; }
-      const unsigned bal = __ballot_sync(0xffffffffu, def);
-      if (def) out[base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u))] = lo + j;
+    if (wdef) {                                           // pass 2 (warp-uniform): publish
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&fl[1], wdef);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (int rd = 0; rd < rounds; ++rd) {
+        const int j = rd * NT + tid;
+        bool def = false;
+        if (j < len) { const float zz = z[j]; def = zz > -INFINITY && zbucket(zz, zmax) < B; }
+        const unsigned bal = __ballot_sync(0xffffffffu, def);
+        if (def) st_relaxed_gpu(&slots[base + __popc(bal & ((1u << lane) - 1u))], lo + j + 1);
+        base += __popc(bal);
+      }
     }
-    __threadfence();
   }
   trace(1, 5);
   cluster_sync_all();                                                   // #2 candidates published
   trace(1, 6);
-  int rc[kSelCL], total = 0, cmax = 0;
+  int rc[kSelCL], total = 0, cmax = 0, off = 0;
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) rc[r] = fallback ? 0 : ld_dsmem_i32(dsmem_addr(&ccnt, r));
 #pragma unroll
-  for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); }
+  for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); off += r < (int)crank ? rc[r] : 0; }
   fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal;
-  int* fl = flags + bh * 4;
-  if (!fallback && crank == 0 && tid == 0) {
-    int nd = 0;
-#pragma unroll
-    for (int r = 0; r < kSelCL; ++r) nd += below[r];
-    fl[1] = nd;
-    st_release_gpu(&fl[0], 1);                           // definite selections ready
-  }
   if (!fallback) {
-    // all ranks' candidates -> local smem; the taken ones (rank < need, larger z first, ties -> lower
-    // index, R12) form a sorted index list used to place every selection
+    // all ranks' candidates -> local smem; each CTA ranks its own (larger z first, ties -> lower
+    // index, R12): rank < need is taken, and the rank is its slot offset in [k - need, k)
     for (int t = tid; t < total; t += NT) {
       int r = 0, base = 0;
 #pragma unroll
@@ -424,32 +411,44 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
     __syncthreads();
     trace(1, 8);
-    for (int t = tid; t < total; t += NT) {
+    for (int t = off + tid; t < off + rc[crank]; t += NT) {
       const uint32_t u = akey[t];
       const int j = aidx[t];
       int rank = 0;
 #pragma unroll 8
       for (int c = 0; c < total; ++c) rank += (akey[c] > u) || (akey[c] == u && aidx[c] < j);
-      tkf[t] = rank < need;
+      if (rank < need) { st_relaxed_gpu(&slots[k - need + rank], j + 1); z[j - lo] = INFINITY; }
     }
-    __syncthreads();
-    for (int t = tid; t < total; t += NT) {
-      if (!tkf[t]) continue;
-      const int j = aidx[t];
-      int ord = 0;                                       // position among the taken, by index
-#pragma unroll 8
-      for (int c = 0; c < total; ++c) ord += tkf[c] && aidx[c] < j;
-      tks[ord] = j;
-      if (j >= lo && j < lo + len) z[j - lo] = INFINITY;
-    }
-    __syncthreads();
     trace(1, 9);
-    if (crank == 0) {                                    // threshold-bucket selections, ascending
-      for (int i = tid; i < need; i += NT) selrest[bh * k + i] = tks[i];
-      __syncthreads();
-      if (tid == 0) { __threadfence(); fl[3] = need; st_release_gpu(&fl[2], 1); }
-    }
     if (sel_user) {          // a3 parity output: the full selection, ascending (R12)
+      __syncthreads();
+      for (int t = tid; t < total; t += NT) {
+        const uint32_t u = akey[t];
+        const int j = aidx[t];
+        int rank = 0;
+        for (int c = 0; c < total; ++c) rank += (akey[c] > u) || (akey[c] == u && aidx[c] < j);
+        tkf[t] = rank < need;
+      }
+      __syncthreads();
+      for (int t = tid; t < total; t += NT) {
+        if (!tkf[t]) continue;
+        const int j = aidx[t];
+        int ord = 0;                                     // position among the taken, by index
+        for (int c = 0; c < total; ++c) ord += tkf[c] && aidx[c] < j;
+        tks[ord] = j;
+      }
+#pragma unroll
+      for (int r = 0; r < kSelCL; ++r) {                 // per-rank count of definite elements
+        const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
+        if (lane == 0) wtmp[warp * kSelCL + r] = v;
+      }
+      __syncthreads();
+      if (tid < kSelCL) { int t = 0; for (int w = 0; w < NW; ++w) t += wtmp[w * kSelCL + tid]; below[tid] = t; }
+      int tot;
+      const int mine = tid < rounds * NW ? wcnt[tid] : 0;
+      const int ex = block_exclusive_scan<NT>(mine, tk, &tot);      // (synchronises the CTA)
+      if (tid < rounds * NW) wcnt[tid] = ex;
+      __syncthreads();
       int base_def = 0;
 #pragma unroll
       for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
@@ -465,14 +464,8 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
         const unsigned bal = __ballot_sync(0xffffffffu, def);
         if (def || taken) {
           const int jj = lo + j;
-          int lo2 = 0;                                    // #taken with index < jj
-          if (nt <= 32) {
-#pragma unroll 8
-            for (int c = 0; c < nt; ++c) lo2 += tks[c] < jj;
-          } else {
-            int hi2 = nt;
-            while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < jj) lo2 = mid + 1; else hi2 = mid; }
-          }
+          int lo2 = 0, hi2 = nt;                          // #taken with index < jj
+          while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < jj) lo2 = mid + 1; else hi2 = mid; }
           sel_user[bh * k + base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u)) + lo2] = jj;
         }
       }
@@ -486,15 +479,17 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     __threadfence();
     cluster_sync_all();
     if (crank == 0) {
-      block_topk_largest<NT>(zg, n, k, out, tk);
+      int32_t* srt = selrest + bh * k;                   // scratch: the top-k, ascending
+      block_topk_largest<NT>(zg, n, k, srt, tk);
       __syncthreads();
-      if (sel_user)
-        for (int i = tid; i < k; i += NT) sel_user[bh * k + i] = out[i];
-      if (tid == 0) {
-        __threadfence();
-        fl[1] = k; fl[3] = 0;
-        st_release_gpu(&fl[2], 1);
-        st_release_gpu(&fl[0], 1);
+      if (tid == 0) ccnt = 0;
+      __syncthreads();
+      for (int i = tid; i < k; i += NT) {
+        const int j = srt[i];
+        if (sel_user) sel_user[bh * k + i] = j;
+        if (!prepub) st_relaxed_gpu(&slots[i], j + 1);
+        else if (zbucket(zg[j], zmax) >= B)               // the definite ones are published already
+          st_relaxed_gpu(&slots[k - need + atomicAdd(&ccnt, 1)], j + 1);
       }
     }
   }
@@ -526,7 +521,7 @@ __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
 template <int G>
 __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int bh, int n_split,
                                               int* __restrict__ counters, int* __restrict__ flags,
-                                              const float* __restrict__ o_part, const float2* __restrict__ ml_part,
+                                              int32_t* __restrict__ slots, const float* __restrict__ o_part, const float2* __restrict__ ml_part,
                                               uint8_t* scratch, uint16_t* __restrict__ out) {
   TRACE_INIT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -614,7 +609,8 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
     __syncthreads();
   }
   trace(2, 7);
-  if (tid == 0) {                                      // leave counter and flags zeroed for the next call
+  for (int i = tid; i < D.k; i += 256) slots[i] = 0;    // leave slots, counter and flags zeroed
+  if (tid == 0) {                                         // for the next call
     counters[bh] = 0;
     int* fl2 = flags + (size_t)bh * 4;
     fl2[0] = 0; fl2[1] = 0; fl2[2] = 0; fl2[3] = 0;
@@ -623,8 +619,8 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
 
 template <int G>
 __global__ void __launch_bounds__(256, 2)
-k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const int32_t* __restrict__ seldef,
-              const int32_t* __restrict__ selrest, int* __restrict__ flags, int step,
+k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t* __restrict__ sel,
+              int* __restrict__ flags, int step,
               float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
               int n_split, float scale, uint16_t* __restrict__ dbg, int* __restrict__ counters,
               uint16_t* __restrict__ out) {
@@ -653,8 +649,12 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
   }
   const int b = bh / D.hk, h = bh - b * D.hk;
   const int split = kind == 0 ? ui : (kind == 1 ? n_sel_u + ui : n_sel_u + n_out_u + ui);
+  int32_t* slots = sel + (size_t)bh * D.k;                     // k_select's unordered selection (id + 1)
+  const int nch = kind == 0 ? min(8, D.k - ui * 8) : 0;        // chunks of a selected-chunk unit (>= 1)
   trace(2, 0);
-  if (tid == 0) { mbar_init(&barAB, 1); mbar_init(&barV, 1); fence_mbar_init(); }
+  if (tid == 0) {   // selected-chunk units: one arrival per chunk-issuing thread
+    mbar_init(&barAB, kind == 0 ? nch : 1); mbar_init(&barV, kind == 0 ? nch : 1); fence_mbar_init();
+  }
   // q is a call input: stage it before waiting on the producer kernels
   for (int i = tid; i < G * kHeadDim; i += 256)
     qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
@@ -668,46 +668,27 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
       asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&barAB)), "r"((uint32_t)bbytes) : "memory");
       bulk_g2s(Bs, Ly.B + (size_t)bh * D.r * kHeadDim, (uint32_t)bbytes, &barAB);
     }
-    // selection published by k_select in two parts: the definite chunks (above the threshold
-    // bucket) as soon as the histogram is known, then the ranked threshold-bucket chunks
-    int* fl = flags + (size_t)bh * 4;
-    const int n_def = cta_wait_flag(&fl[0]), nd_u = (n_def + 7) >> 3;
-    trace(2, 1);
-    const int32_t* list;
-    int nch;
-    if (ui < nd_u) { list = seldef + (size_t)bh * D.k + ui * 8; nch = min(8, n_def - ui * 8); }
-    else {
-      const int n_rest = cta_wait_flag(&fl[2]), u2 = ui - nd_u;
-      list = selrest + (size_t)bh * D.k + u2 * 8;
-      nch = max(0, min(8, n_rest - u2 * 8));
-    }
-    ntok = nch * kChunk;
-    if (ntok == 0) {                                     // spare unit slot: empty partial
-      for (int hq = tid >> 7; hq < G; hq += 2) {
-        const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-        o_part[row * kHeadDim + (tid & 127)] = 0.f;
-        if ((tid & 127) == 0) ml_part[row] = make_float2(-INFINITY, 0.f);
-      }
-      if (tid == 0) mbar_arrive_plain(&barAB);          // B_h was expected without an arrival
-      mbar_wait(&barAB, 0);                              // retire the B_h copy before leaving
-      sparse_finish<G>(D, b, h, bh, n_split, counters, flags, o_part, ml_part, smem + lay.a, out);
-      return;
-    }
-    if (tid < kUnitTok) tok[tid] = tid < ntok ? list[tid >> 3] * kChunk + (tid & 7) : 0;
-    const uint32_t rb = kChunk * D.r * 2;
-    if (tid == 0) {                                      // arm both barriers before any copy is issued
-      mbar_expect_tx(&barAB, nch * rb);
-      mbar_expect_tx(&barV, nch * kChunk * kHeadDim * 2);
-    }
-    __syncwarp();
-    if (tid < nch) {                                     // one issuing thread per chunk
-      const int id = list[tid];
-      // a4 operands first (HBM, needed first): 8 contiguous factor rows (2.5 KB at r = 160)
+    // thread c < nch waits for its slot, then issues its chunk's two copies at once: the value fetch
+    // of each chunk starts the moment k_select publishes it
+    if (tid < nch) {
+      const int* sp = slots + ui * 8 + tid;
+      int v;
+      while ((v = ld_relaxed_gpu(sp)) == 0) __nanosleep(32);
+      const int id = v - 1;
+#pragma unroll
+      for (int e = 0; e < kChunk; ++e) tok[tid * kChunk + e] = id * kChunk + e;
+      const uint32_t rb = kChunk * D.r * 2;
+      // a4 operands (HBM): 8 contiguous factor rows (2.5 KB at r = 160)
+      mbar_expect_tx(&barAB, rb);
       bulk_g2s(As + tid * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)id * kChunk) * D.r, rb, &barAB);
       // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy)
+      mbar_expect_tx(&barV, kChunk * kHeadDim * 2);
       bulk_g2s(Vs + tid * kChunk * kHeadDim, Ly.V_host + ((size_t)bh * D.s + (size_t)id * kChunk) * kHeadDim,
                kChunk * kHeadDim * 2, &barV);
+    } else if (tid < kUnitTok && tid >= nch * kChunk) {
+      tok[tid] = 0;                                      // padded rows (masked below)
     }
+    ntok = nch * kChunk;
     trace(2, 2);
     __syncthreads();
     mbar_wait(&barAB, 0);
@@ -763,20 +744,22 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
         }
       }
     }
-    if (dbg) {                        // a4 parity hook: bf16 of the fp32 keys at the chunk's rank in
-      const int n_rest = cta_wait_flag(&fl[2]);   // the ascending selection (= #definite + #rest below)
-      const int32_t* dl = seldef + (size_t)bh * D.k;
-      const int32_t* rl = selrest + (size_t)bh * D.k;
+    if (dbg) {   // a4 parity hook: bf16 of the fp32 keys at the chunk's rank in the ascending selection
+      __syncthreads();                                   // A rows consumed: reuse their smem for the ids
+      int* ids = reinterpret_cast<int*>(As);
+      for (int i = tid; i < D.k; i += 256) {
+        int v;
+        while ((v = ld_relaxed_gpu(slots + i)) == 0) __nanosleep(32);
+        ids[i] = v - 1;
+      }
+      __syncthreads();
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = ty + 16 * i;
         if (row < ntok) {
           const int cid = tok[row] >> 3;
-          int lo2 = 0, hi2 = n_def;
-          while (lo2 < hi2) { const int m = (lo2 + hi2) >> 1; if (dl[m] < cid) lo2 = m + 1; else hi2 = m; }
-          int lo3 = 0, hi3 = n_rest;
-          while (lo3 < hi3) { const int m = (lo3 + hi3) >> 1; if (rl[m] < cid) lo3 = m + 1; else hi3 = m; }
-          const int pos = lo2 + lo3;
+          int pos = 0;
+          for (int c = 0; c < D.k; ++c) pos += ids[c] < cid;
           uint4 kb = make_uint4(pack_bf2(acc[i][0], acc[i][1]), pack_bf2(acc[i][2], acc[i][3]),
                                 pack_bf2(acc[i][4], acc[i][5]), pack_bf2(acc[i][6], acc[i][7]));
           *reinterpret_cast<uint4*>(dbg + (((size_t)bh * D.k + pos) * kChunk + (row & 7)) * kHeadDim + tx * 8) = kb;
@@ -864,7 +847,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, const in
     o_part[row * kHeadDim + d] = a;
     if (d == 0) ml_part[row] = ml[hq];
   }
-  sparse_finish<G>(D, b, h, bh, n_split, counters, flags, o_part, ml_part, smem + lay.a, out);
+  sparse_finish<G>(D, b, h, bh, n_split, counters, flags, slots, o_part, ml_part, smem + lay.a, out);
 }
 
 // =============================================================================================
@@ -879,7 +862,7 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
   size_t off = ws_header_bytes(D);                  // zero-initialised per-(b,h) counters live first
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return base + o; };
   const int tph = tiles_per_head(D);
-  const int n_sel_u = (D.k + 7) / 8 + 1, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+  const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
   const int n_win_max = (D.wcap + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_max;
   const size_t BHq = (size_t)D.b * D.hq, BHk = (size_t)D.b * D.hk;
@@ -955,7 +938,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   const int tph = ws.n_sblk;
   const int total_tiles = D.b * D.hk * tph;
   {
-    const int nsu = (D.k + 7) / 8 + 1, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+    const int nsu = (D.k + 7) / 8, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
     const int nsp = nsu + nou + (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
     if (nsp > 32 * kMergeMaxPerLane || (size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 > (size_t)(lay.q - lay.a))
       return cudaErrorInvalidConfiguration;                                           // merge scratch
@@ -993,13 +976,12 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
   }
-  // definite + threshold-bucket chunks may straddle one extra 8-chunk unit
-  const int n_sel_u = (D.k + 7) / 8 + 1, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
+  const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
   const int n_win_u = (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_u;
   const int units = D.b * D.hk * n_split;
   if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
-                      (const int32_t*)ws.sel, (const int32_t*)ws.selrest, ws.flags, step, ws.o_part, ws.ml_part,
+                      ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
                       n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, ws.counters, out))) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
   *launches += 3;

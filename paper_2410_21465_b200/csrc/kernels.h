@@ -32,12 +32,12 @@ struct BuildWs {
 };
 struct DecodeWs {
   int* counters;     // [b][hk] zero-initialised by the caller once; every call leaves them zero
-  int* flags;        // [b][hk][4] {def_ready, n_def, rest_ready, n_rest}; zeroed again by each call's merger
-  int32_t* selrest;  // [b][hk][k] threshold-bucket selections, ascending
+  int* flags;        // [b][hk][4] {score_done, slots_reserved, -, -}; zeroed again by each call's merger
+  int32_t* selrest;  // [b][hk][k] radix-fallback scratch (top-k, ascending)
   float* logits;     // [b][hq][n_c]
   float2* part;      // [b][hq][kSegMax] per-(score CTA, head) softmax partials (max, sumexp)
   float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
-  int32_t* sel;      // [b][hk][k]
+  int32_t* sel;      // [b][hk][k] published selection, unordered, chunk id + 1 (0 = not yet); re-zeroed
   float* o_part;     // [b][hq][n_split][d]
   float2* ml_part;   // [b][hq][n_split]
   int n_sblk, n_split;
