@@ -2,6 +2,7 @@
 // and kernel orchestration.  Host-side only; kernels live in build.cu / decode.cu.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstring>
 #include <string>
@@ -13,6 +14,8 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+bool g_trace_on = false;       // tuning: trace buffer installed
+int g_trace_calls = 0;
 
 skv_status fail(skv_status st, const char* fmt, ...) {
   char buf[512];
@@ -53,7 +56,7 @@ skv_status check_dims(const skv_dims* d, skv::Dims* D) {
   if (d->window_cap < w_eff || d->window_cap < 1)
     return fail(SKV_EINVAL, "window_cap %d < w_eff %d", d->window_cap, w_eff);
   *D = skv::Dims{d->batch, d->n_q_heads, d->n_kv_heads, g, d->head_dim, d->ctx_len, d->rank, d->chunk,
-                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff};
+                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff, 0};
   return SKV_OK;
 }
 
@@ -162,6 +165,8 @@ skv_status shadowkv_profile_end(double* total_ms, int32_t* counts) {
 
 
 skv_status shadowkv_trace_buffer(void* dev_buf) {
+  g_trace_on = dev_buf != nullptr;
+  g_trace_calls = 0;
   cudaError_t e = skv::set_trace_buffer(dev_buf);
   if (e == cudaSuccess) e = skv::set_trace_buffer_tc(dev_buf);
   if (e != cudaSuccess) return fail(SKV_ECUDA, "trace buffer: %s", cudaGetErrorString(e));
@@ -224,6 +229,11 @@ skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, cons
     return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
   skv::DecodeWs ws;
   skv::decode_ws_bytes(D, &ws, static_cast<char*>(workspace));
+  if (g_trace_on) {          // consecutive calls stamp consecutive trace blocks (SKV_TRACE_SLOTS, default 1)
+    const char* ns = getenv("SKV_TRACE_SLOTS");
+    const int n = ns ? atoi(ns) : 1;
+    D.trace_slot = n > 1 ? g_trace_calls++ % n : 0;
+  }
   int launches = 0;
   cudaError_t e = skv::launch_decode(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws,
                                      static_cast<cudaStream_t>(stream), &launches, g_prof);

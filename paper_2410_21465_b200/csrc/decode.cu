@@ -25,14 +25,13 @@
 
 namespace skv {
 
-constexpr int kMergeMaxPerLane = 16;   // merge handles n_split <= 512 partial units per (b, h)
 constexpr int kMergeHeads = 4;         // heads whose partial loads are in flight together
 
 
 // optional per-CTA timeline (globaltimer ns) for tuning: [kernel][block < 4096][event < 16]
 __device__ uint64_t* g_trace = nullptr;
 // kernels read g_trace once (TRACE_INIT) so that disabled tracing costs no dependent loads
-#define TRACE_INIT uint64_t* const trace_buf_ = g_trace
+#define TRACE_INIT uint64_t* const trace_buf_ = g_trace ? g_trace + (size_t)D.trace_slot * kTraceSlot : nullptr
 #define trace(kernel, ev)                                                                            \
   do {                                                                                               \
     if (trace_buf_ != nullptr && threadIdx.x == 0)                                                   \
@@ -528,6 +527,7 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
   // ---- the last unit of this (b, h) to finish merges all partials (log-sum-exp) -> out
   __shared__ int is_last;
   __syncthreads();                                     // all partial stores of this CTA issued
+  trace(2, 9);
   if (tid == 0) {
     __threadfence();                                   // cumulative release of the CTA's partials
     is_last = atomicAdd(&counters[bh], 1) == n_split - 1;
@@ -538,51 +538,51 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
   if (!is_last) return;
   float* wsm = reinterpret_cast<float*>(scratch);          // [G][n_split] weights (A/B region is free)
   trace(3, 0);
-  for (int hq = warp; hq < G; hq += 8) {
-    const float2* mlr = ml_part + ((size_t)b * D.hq + (size_t)h * G + hq) * n_split;
-    float2 v[kMergeMaxPerLane];
+  // o_hq = sum_s w_s o_s: thread = (split group sg of 8, float4 dims); the first batch of partial
+  // loads is issued before the weights are known (independent), so the two L2 trips overlap
+  const int d4 = (tid & 31) * 4, sg = tid >> 5;
+  const int nper = (n_split - sg + 7) / 8;                      // splits of this group
+  auto load_batch = [&](int h0, int u0, float4 (&vv)[kMergeHeads][4]) {
 #pragma unroll
-    for (int u = 0; u < kMergeMaxPerLane; ++u) {
-      const int s2 = lane + 32 * u;
-      v[u] = s2 < n_split ? __ldcg(&mlr[s2]) : make_float2(-INFINITY, 0.f);
+    for (int x = 0; x < kMergeHeads; ++x) {
+      const size_t row = (size_t)b * D.hq + (size_t)h * G + h0 + x;
+      const float4* opr = reinterpret_cast<const float4*>(o_part + row * n_split * kHeadDim + d4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s2 = sg + 8 * (u0 + u);
+        vv[x][u] = (u0 + u < nper && h0 + x < G) ? __ldcg(opr + (size_t)s2 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
+  };
+  float4 vfirst[kMergeHeads][4];
+  load_batch(0, 0, vfirst);
+  // weights w_s = exp(m_s - M) / sum_s' l_s' exp(m_s' - M) per head, from the (m, l) partials
+  float2* mls = reinterpret_cast<float2*>(wsm + ((G * n_split + 3) & ~3) + kMergeHeads * 8 * kHeadDim);
+  const float2* mlb = ml_part + ((size_t)b * D.hq + (size_t)h * G) * n_split;
+  for (int i = tid; i < G * n_split; i += 256) mls[i] = __ldcg(&mlb[i]);
+  __syncthreads();
+  for (int hq = warp; hq < G; hq += 8) {
+    const float2* mr = mls + hq * n_split;
     float M = -INFINITY;
-#pragma unroll
-    for (int u = 0; u < kMergeMaxPerLane; ++u) M = fmaxf(M, v[u].x);
+    for (int s2 = lane; s2 < n_split; s2 += 32) M = fmaxf(M, mr[s2].x);
     M = warp_max(M);
     float Ls = 0.f;
-#pragma unroll
-    for (int u = 0; u < kMergeMaxPerLane; ++u) { v[u].x = expf(v[u].x - M); Ls = fmaf(v[u].y, v[u].x, Ls); }
+    for (int s2 = lane; s2 < n_split; s2 += 32) { const float2 v = mr[s2]; if (v.x > -INFINITY) Ls = fmaf(v.y, expf(v.x - M), Ls); }
     const float inv = 1.f / warp_sum(Ls);
-#pragma unroll
-    for (int u = 0; u < kMergeMaxPerLane; ++u) {
-      const int s2 = lane + 32 * u;
-      if (s2 < n_split) wsm[hq * n_split + s2] = v[u].x * inv;
+    for (int s2 = lane; s2 < n_split; s2 += 32) {
+      const float mx = mr[s2].x;
+      wsm[hq * n_split + s2] = mx > -INFINITY ? expf(mx - M) * inv : 0.f;
     }
   }
   __syncthreads();
   trace(3, 1);
-  // o_hq = sum_s w_s o_s: thread = (split group sg of 8, float4 dims); every head's loads in flight
   float* red = wsm + ((G * n_split + 3) & ~3);                  // [kMergeHeads][8][128]
-  const int d4 = (tid & 31) * 4, sg = tid >> 5;
-  const int nper = (n_split - sg + 7) / 8;                      // splits of this group
 #pragma unroll
   for (int h0 = 0; h0 < G; h0 += kMergeHeads) {
     float4 a[kMergeHeads];
 #pragma unroll
     for (int x = 0; x < kMergeHeads; ++x) a[x] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int u0 = 0; u0 < nper; u0 += 4) {
-      float4 vv[kMergeHeads][4];
-#pragma unroll
-      for (int x = 0; x < kMergeHeads; ++x) {
-        const size_t row = (size_t)b * D.hq + (size_t)h * G + h0 + x;
-        const float4* opr = reinterpret_cast<const float4*>(o_part + row * n_split * kHeadDim + d4);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int s2 = sg + 8 * (u0 + u);
-          vv[x][u] = (u0 + u < nper && h0 + x < G) ? __ldcg(opr + (size_t)s2 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
+    auto fma_batch = [&](int u0, const float4 (&vv)[kMergeHeads][4]) {
 #pragma unroll
       for (int x = 0; x < kMergeHeads; ++x)
 #pragma unroll
@@ -592,6 +592,13 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
           a[x].x = fmaf(w, vv[x][u].x, a[x].x); a[x].y = fmaf(w, vv[x][u].y, a[x].y);
           a[x].z = fmaf(w, vv[x][u].z, a[x].z); a[x].w = fmaf(w, vv[x][u].w, a[x].w);
         }
+    };
+    int u0 = 0;
+    if (h0 == 0) { fma_batch(0, vfirst); u0 = 4; }
+    for (; u0 < nper; u0 += 4) {
+      float4 vv[kMergeHeads][4];
+      load_batch(h0, u0, vv);
+      fma_batch(u0, vv);
     }
 #pragma unroll
     for (int x = 0; x < kMergeHeads; ++x)
@@ -623,7 +630,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
               int* __restrict__ flags, int step,
               float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
               int n_split, float scale, uint16_t* __restrict__ dbg, int* __restrict__ counters,
-              uint16_t* __restrict__ out) {
+              uint16_t* __restrict__ out, int early_next) {
   TRACE_INIT;
   extern __shared__ __align__(128) uint8_t smem[];
   const AttnSmem lay = attn_smem_layout(D.r, G);
@@ -689,6 +696,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       tok[tid] = 0;                                      // padded rows (masked below)
     }
     ntok = nch * kChunk;
+    if (early_next) pdl_trigger();                       // next layer's score may become resident
     trace(2, 2);
     __syncthreads();
     mbar_wait(&barAB, 0);
@@ -768,6 +776,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     }
   } else {
     // ---- outlier or window (R8, R18) unit: exact keys and values from HBM
+    if (early_next) pdl_trigger();
     cta_wait_flag(&flags[(size_t)bh * 4]);              // (score's window append is visible)
     const uint16_t *Ksrc, *Vsrc;
     if (kind == 1) {
@@ -839,14 +848,30 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   mbar_wait(&barV, 0);                                   // values (from PCIe for selected units)
   trace(2, 5);
   __syncthreads();
-  // ---- PV: thread = (dim, head parity)
-  for (int hq = hh; hq < G; hq += 2) {
-    float a = 0.f;
-    for (int t = 0; t < ntok; ++t) a = fmaf(P[hq * kUnitTok + t], bf2f(Vs[t * kHeadDim + d]), a);
-    const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-    o_part[row * kHeadDim + d] = a;
-    if (d == 0) ml_part[row] = ml[hq];
+  // ---- PV: thread = (dim pair, head group of 4): bf16x2 value loads, float4 probability loads
+  {
+    const int dp = tid & 63, grp = tid >> 6;
+    const int ntok4 = (ntok + 3) & ~3;                   // P is 0 past ntok; stale V rows are skipped
+    for (int hq = grp; hq < G; hq += 4) {
+      const float* ph = P + hq * kUnitTok;
+      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+      for (int t = 0; t < ntok4; t += 4) {
+        const float4 p4 = *reinterpret_cast<const float4*>(ph + t);
+        const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t v2 = t + e < ntok ? *reinterpret_cast<const uint32_t*>(Vs + (t + e) * kHeadDim + 2 * dp) : 0u;
+          float2& a = (e & 1) ? a1 : a0;
+          a.x = fmaf(pp[e], bf_lo(v2), a.x);
+          a.y = fmaf(pp[e], bf_hi(v2), a.y);
+        }
+      }
+      const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+      *reinterpret_cast<float2*>(o_part + row * kHeadDim + 2 * dp) = make_float2(a0.x + a1.x, a0.y + a1.y);
+      if (dp == 0) ml_part[row] = ml[hq];
+    }
   }
+  trace(2, 8);
   sparse_finish<G>(D, b, h, bh, n_split, counters, flags, slots, o_part, ml_part, smem + lay.a, out);
 }
 
@@ -940,7 +965,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   {
     const int nsu = (D.k + 7) / 8, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
     const int nsp = nsu + nou + (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
-    if (nsp > 32 * kMergeMaxPerLane || (size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 > (size_t)(lay.q - lay.a))
+    if ((size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 + (size_t)G * nsp * 8 > (size_t)(lay.q - lay.a))
       return cudaErrorInvalidConfiguration;                                           // merge scratch
   }
   int grid_s = total_tiles < 2 * num_sms() ? total_tiles : 2 * num_sms();
@@ -980,9 +1005,13 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   const int n_win_u = (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_u;
   const int units = D.b * D.hk * n_split;
+  // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score
+  // grid then launches only when this grid drains)
+  const char* stg = getenv("SKV_SPARSE_TRIGGER");
+  const int early_next = (stg && stg[0] == '0') ? 0 : 1;
   if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
                       ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
-                      n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, ws.counters, out))) return e;
+                      n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, ws.counters, out, early_next))) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
   *launches += 3;
   return cudaGetLastError();

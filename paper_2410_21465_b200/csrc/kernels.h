@@ -9,7 +9,9 @@ namespace skv {
 struct Dims {          // validated, derived sizes
   int b, hq, hk, g, d, s, r, c, o, k, w, wcap;
   int n_c, w_eff;
+  int trace_slot;      // tuning only: which [4][4096][16] block of the trace buffer this call stamps
 };
+constexpr size_t kTraceSlot = (size_t)4 * 4096 * 16;
 
 struct Rope {
   const float* inv_freq;

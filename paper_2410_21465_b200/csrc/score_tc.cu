@@ -118,7 +118,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   const int t_end = (int)((long long)(blockIdx.x + 1) * total / gridDim.x);
   const int ntile = t_end - t_begin;
   const int bh0 = t_begin / tiles_per_head;
-  uint64_t* const trace_buf = g_trace_tc;
+  uint64_t* const trace_buf = g_trace_tc ? g_trace_tc + (size_t)D.trace_slot * kTraceSlot : nullptr;
   trace_tc(trace_buf, 0);
   if (early_trigger) pdl_trigger();
   // the producer thread initialises the barriers and puts the first kTcStages tiles in flight
@@ -133,7 +133,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" :: "r"(smem_u32(&tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  pdl_wait();                                          // everything below may read the caller's inputs
+  // landmarks are layer state written by build_cache, never by a decode-step kernel: the first ring
+  // fills do not depend on the preceding grid and stream while it drains (PDL prologue)
   if (tid == 4 * 32 && ntile > 0) {
     for (int i = 0; i < ntile && i < kTcStages; ++i) {
       const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
@@ -143,6 +144,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       tma_load_2d(sA + i * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[i]);
     }
   }
+  pdl_wait();                                          // everything below may read the caller's inputs
   if (ntile <= 0) return;
   const int nheads = (t_end - 1) / tiles_per_head - bh0 + 1;          // <= kTcMaxHeads (host check)
   // setup with every global load issued before any dependent use:

@@ -16,7 +16,9 @@ from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace,
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--layers", type=int, default=4)
+ap.add_argument("--slots", type=int, default=1, help="trace this many consecutive layers (steady state)")
 args = ap.parse_args()
+os.environ["SKV_TRACE_SLOTS"] = str(args.slots)
 cfg = synth.CONFIGS[args.config]
 shape = Shape.from_config(cfg, steps=64)
 inv, rot, il = synth.rope_table(cfg)
@@ -30,23 +32,39 @@ for l in range(args.layers):
     st.build(rope.struct, ws)
     states.append(st)
 out = torch.empty(cfg.batch, cfg.n_q_heads, 128, dtype=torch.bfloat16, device="cuda")
-tr = torch.zeros(4 * 4096 * 16, dtype=torch.int64, device="cuda")
+SLOT = 4 * 4096 * 16
+tr = torch.zeros(args.slots * SLOT, dtype=torch.int64, device="cuda")
+first = args.layers - args.slots
+sis = [[synth.gen_step(cfg, 99, l, step, device="cuda") for l in range(args.layers)] for step in range(6)]
 for step in range(6):
     for l, st in enumerate(states):
-        si = synth.gen_step(cfg, 99, l, step, device="cuda")
-        if step == 5 and l == args.layers - 1:
+        si = sis[step][l]
+        if step == 5 and l == first:
             torch.cuda.synchronize()
             tr.zero_()
             bd.shadowkv_trace_buffer(tr)
         st.decode(rope.struct, si["q"], si["k_new"], si["v_new"], step, out, ws)
-        if step == 5 and l == args.layers - 1:
-            torch.cuda.synchronize()
-            bd.shadowkv_trace_buffer(None)
-t = tr.view(4, 4096, 16).cpu().numpy().astype(np.float64)
+    if step == 5:
+        torch.cuda.synchronize()
+        bd.shadowkv_trace_buffer(None)
+T = tr.view(args.slots, 4, 4096, 16).cpu().numpy().astype(np.float64)
+g0 = T[0, 0][T[0, 0][:, 0] > 0][:, 0].min()
+if args.slots > 1:
+    print("== per-layer milestones (us from the first traced layer's score start)")
+    print("   layer  score_start score_end  sel_start  pub(cand)  first_issue  p50_issue  last_V_in  merge_end")
+    for sl in range(args.slots):
+        t = T[sl]
+        def col(k, e, f):
+            c = t[k][:, e]; c = c[c > 0]
+            return f(c - g0) / 1e3 if len(c) else float("nan")
+        print(f"   {sl:5d}  {col(0, 0, np.min):10.2f} {col(0, 1, np.max):9.2f} {col(1, 0, np.min):10.2f} "
+              f"{col(1, 5, np.max):10.2f} {col(2, 2, np.min):11.2f} {col(2, 2, np.median):10.2f} "
+              f"{col(2, 5, np.max):10.2f} {col(2, 7, np.max):10.2f}")
+t = T[args.slots - 1]
 t0 = t[0][t[0][:, 0] > 0][:, 0].min()
 names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "-", "-", "emitted", "nseg", "loaded_max", "exp_sum"],
          3: ["merge_start", "weights"],
-         2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end"]}
+         2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end", "pv_done", "synced"]}
 for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
     m = t[kid]
     rows = m[m[:, 0] > 0]
