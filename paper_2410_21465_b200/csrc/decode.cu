@@ -217,8 +217,10 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
 // =============================================================================================
 // a2 + a3: normalise, group max, exact top-k
 // =============================================================================================
-__device__ __forceinline__ int zbucket(float z, float zmax) {   // 0 = highest scores; 255 = catch-all
-  return min(255, (int)floorf((zmax - z) * 32.f));
+// 0 = highest scores; 255 = catch-all.  zmax comes from the score partials' running max, which may
+// sit an ulp off the largest z: clamp, so every z maps into [0, 255] the same way in every pass
+__device__ __forceinline__ int zbucket(float z, float zmax) {
+  return min(255, max(0, (int)floorf((zmax - z) * 32.f)));
 }
 
 // One cluster of kSelCL CTAs per (request, KV head); CTA `rank` owns landmarks
@@ -241,13 +243,14 @@ template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 1)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
          int score_total, int score_grid, float* __restrict__ zws, int32_t* __restrict__ sel,
-         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int early_trigger) {
+         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int early_trigger,
+         int force_fb) {
   TRACE_INIT;
   constexpr int NT = kSelThreads, NW = NT / 32;
   extern __shared__ __align__(16) float zdyn[];
   __shared__ TopKSmem<NT> tk;
   __shared__ float lse[G], hm[G];
-  __shared__ int hist[256], ghist[256], below[kSelCL], info[4];
+  __shared__ int hist[256], ghist[256], below[kSelCL], info[4], wdefs[NT / 32];
   __shared__ int cidx[kSelCandLocal], ccnt;
   __shared__ uint32_t ckey[kSelCandLocal];
   __shared__ int aidx[kSelCandLocal];
@@ -357,7 +360,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   // [k - need, k) once ranked.  Each sparse-attention unit polls its own 8 slots.
   int32_t* slots = sel + bh * k;
   const int rounds = (len + NT - 1) / NT;
-  const bool prepub = !(B == 255 || n_per > 16384);       // else: radix fallback publishes all k
+  const bool prepub = !(B == 255 || n_per > 16384 || force_fb == 1);  // else: radix fallback publishes all k
   bool fallback = !prepub;
   if (prepub) {
     int wdef = 0;                                         // pass 1: candidates + definite count
@@ -374,10 +377,24 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       if (lane == 0) wcnt[rd * NW + warp] = c;
       wdef += c;
     }
+    // deterministic slot positions (the summation order of the output must not depend on timing):
+    // [ranks below this one][warps below this one][rounds][lanes].  A rank's definite count is its
+    // histogram mass above bucket B, summed from the per-rank histograms already in registers.
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r) {
+      const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
+      if (lane == 0) wtmp[warp * kSelCL + r] = v;
+    }
+    if (lane == 0) wdefs[warp] = wdef;
+    __syncthreads();
     if (wdef) {                                           // pass 2 (warp-uniform): publish
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&fl[1], wdef);
-      base = __shfl_sync(0xffffffffu, base, 0);
+      int base = 0;                                       // lane w sums warp w's share, then reduce
+      if (lane < NW) {
+        base = lane < warp ? wdefs[lane] : 0;
+#pragma unroll
+        for (int r = 0; r < kSelCL; ++r) base += r < (int)crank ? wtmp[lane * kSelCL + r] : 0;
+      }
+      base = __reduce_add_sync(0xffffffffu, base);
       for (int rd = 0; rd < rounds; ++rd) {
         const int j = rd * NT + tid;
         bool def = false;
@@ -396,7 +413,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   for (int r = 0; r < kSelCL; ++r) rc[r] = fallback ? 0 : ld_dsmem_i32(dsmem_addr(&ccnt, r));
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); off += r < (int)crank ? rc[r] : 0; }
-  fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal;
+  fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal || force_fb == 2;
   if (!fallback) {
     // all ranks' candidates -> local smem; each CTA ranks its own (larger z first, ties -> lower
     // index, R12): rank < need is taken, and the rank is its slot offset in [k - need, k)
@@ -436,12 +453,6 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
         for (int c = 0; c < total; ++c) ord += tkf[c] && aidx[c] < j;
         tks[ord] = j;
       }
-#pragma unroll
-      for (int r = 0; r < kSelCL; ++r) {                 // per-rank count of definite elements
-        const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
-        if (lane == 0) wtmp[warp * kSelCL + r] = v;
-      }
-      __syncthreads();
       if (tid < kSelCL) { int t = 0; for (int w = 0; w < NW; ++w) t += wtmp[w * kSelCL + tid]; below[tid] = t; }
       int tot;
       const int mine = tid < rounds * NW ? wcnt[tid] : 0;
@@ -481,14 +492,17 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       int32_t* srt = selrest + bh * k;                   // scratch: the top-k, ascending
       block_topk_largest<NT>(zg, n, k, srt, tk);
       __syncthreads();
-      if (tid == 0) ccnt = 0;
-      __syncthreads();
-      for (int i = tid; i < k; i += NT) {
-        const int j = srt[i];
-        if (sel_user) sel_user[bh * k + i] = j;
-        if (!prepub) st_relaxed_gpu(&slots[i], j + 1);
-        else if (zbucket(zg[j], zmax) >= B)               // the definite ones are published already
-          st_relaxed_gpu(&slots[k - need + atomicAdd(&ccnt, 1)], j + 1);
+      for (int i = tid; i < k && sel_user; i += NT) sel_user[bh * k + i] = srt[i];
+      if (warp == 0) {                                   // publish in ascending order (deterministic)
+        int base = prepub ? k - need : 0;                // the definite ones are published already
+        for (int i0 = 0; i0 < k; i0 += 32) {
+          const int i = i0 + lane;
+          const int j = i < k ? srt[i] : 0;
+          const bool pub = i < k && (!prepub || zbucket(zg[j], zmax) >= B);
+          const unsigned bal = __ballot_sync(0xffffffffu, pub);
+          if (pub) st_relaxed_gpu(&slots[base + __popc(bal & ((1u << lane) - 1u))], j + 1);
+          base += __popc(bal);
+        }
       }
     }
   }
@@ -990,14 +1004,16 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   {
     const char* et = getenv("SKV_EARLY_TRIGGER");         // tuning hook: 1 = PDL trigger at kernel start
     const int early_sel = (et && et[0] == '1') ? 1 : 0;
+    const char* fb = getenv("SKV_SELECT_FALLBACK");       // test hook: 1 / 2 force the radix fallback
+    const int force_fb = fb ? atoi(fb) : 0;               // before / after the definite chunks publish
     const bool zsm = z_fits_smem(D, G);
     const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
     if (zsm) e = launch_pdl(k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                             (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
-                            ws.sel, ws.selrest, ws.flags, sel_ids, early_sel);
+                            ws.sel, ws.selrest, ws.flags, sel_ids, early_sel, force_fb);
     else e = launch_pdl(k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                         (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
-                        ws.sel, ws.selrest, ws.flags, sel_ids, early_sel);
+                        ws.sel, ws.selrest, ws.flags, sel_ids, early_sel, force_fb);
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
   }

@@ -4,11 +4,15 @@
 //
 // One UMMA per 16-wide k step: M = 128 landmark rows (A, K-major, SWIZZLE_128B, streamed from HBM
 // by TMA in two 64-column boxes), N = 16 query heads of the GQA group (B, zero-padded, built once
-// per KV head in smem), K = 128 = head_dim, fp32 accumulators in TMEM (2 x 16 columns, double
-// buffered).  Warp roles (192 threads): warps 0-3 epilogue (TMEM lane quadrant = warp), warp 4
-// TMA producer, warp 5 MMA issuer.  The epilogue reads each landmark's G logits with tcgen05.ld,
-// masks outlier chunks (R3), writes the scaled logits and a per-(tile, quadrant) softmax partial
-// (max, sum exp) that k_select merges into the exact per-head log-sum-exp.
+// per KV head in smem), K = 128 = head_dim, fp32 accumulators in TMEM (8 x 16 columns).  Warp
+// roles (224 threads): warps 0-3 epilogue (TMEM lane quadrant = warp), warp 4 TMA producer,
+// warps 5-6 MMA issuers on alternate tiles (measured: one issuing thread is paced at ~70 cycles
+// per tcgen05.mma at any N <= 128, two on different sub-partitions reach ~40, the rate at which
+// the tensor core reads the 4 KB A operand from smem; tools/probe_umma.cu).  The epilogue reads
+// each landmark's G logits with tcgen05.ld, masks outlier chunks (R3), writes the scaled logits
+// and per-(CTA, KV head) softmax partials (max, sum exp) that k_select merges into the exact
+// per-head log-sum-exp.  The first ring fills are issued before griddepcontrol.wait: landmarks
+// are layer state that no decode-step kernel writes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -25,7 +29,7 @@ constexpr int kTcStages = 6;
 constexpr int kTcAcc = 8;                 // TMEM accumulator buffers (16 fp32 columns each)
 constexpr int kTcMaxHeads = 4;            // KV heads a CTA's contiguous tile range may touch
 constexpr int kTcMaxTiles = 64;           // tiles per CTA (bitmap size); host sizes the grid accordingly
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 224;         // 4 epilogue warps, 1 TMA producer, 2 MMA issuers
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
 
@@ -212,10 +216,11 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         tma_load_2d(sA + s * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[s]);
       }
     }
-  } else if (warp == 5) {
-    // ---------------- MMA issuer (single thread) ----------------
+  } else if (warp == 5 || warp == 6) {
+    // ---------------- MMA issuers: one thread each on two SM sub-partitions, alternating tiles ----------
+    // (a single issuing thread is paced at ~70 cycles per tcgen05.mma; two overlap to the smem-read bound)
     if (lane == 0) {
-      for (int i = 0; i < ntile; ++i) {
+      for (int i = warp - 5; i < ntile; i += 2) {
         const int s = i % kTcStages, ph = (i / kTcStages) & 1, buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
         mbar_wait(&full[s], ph);
         if (i < 4) trace_tc_any(trace_buf, 2 + i);                  // tile i landed in smem
@@ -231,6 +236,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         }
         umma_commit(&empty[s]);          // smem stage may be refilled once these MMAs retire
         umma_commit(&acc_full[buf]);     // accumulator ready for the epilogue
+        if (i == 0) trace_tc_any(trace_buf, 12);                    // tile 0's MMAs issued
       }
     }
   } else {
@@ -238,20 +244,22 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     // per-thread online softmax partials over the CTA's rows of each KV head, merged across the 4
     // epilogue warps once per head segment: one partial per (CTA, KV head) at slot = CTA index minus
     // the first CTA that covers the head (seg_first(); k_select recomputes the same mapping)
+    // Branch-free online update in the log2 domain, one independent chain per head (ILP): the four
+    // epilogue warps sit one per sub-partition, so dependent latency, not issue, paces them.
+    // A finite floor stands in for -inf so that fully masked rows never produce inf - inf.
+    constexpr float kFloor = -1e30f, kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
     float m_run[G], s_run[G];
 #pragma unroll
-    for (int hq = 0; hq < G; ++hq) { m_run[hq] = -INFINITY; s_run[hq] = 0.f; }
-    int cur_bh = t_begin / tiles_per_head;
+    for (int hq = 0; hq < G; ++hq) { m_run[hq] = kFloor; s_run[hq] = 0.f; }
     auto flush = [&](int bh) {
       const int b = bh / D.hk, h = bh - b * D.hk;
       const int slot = (int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x);
 #pragma unroll
       for (int hq = 0; hq < G; ++hq) {
-        const float m = warp_max(m_run[hq]);
-        const float sc = (m > -INFINITY && m_run[hq] > -INFINITY) ? s_run[hq] * expf(m_run[hq] - m) : 0.f;
-        const float sm = warp_sum(sc);
-        if (lane == 0) wpart[warp][hq] = make_float2(m, sm);
-        m_run[hq] = -INFINITY; s_run[hq] = 0.f;
+        const float m2 = warp_max(m_run[hq]);
+        const float sm = warp_sum(s_run[hq] * exp2f(m_run[hq] - m2));
+        if (lane == 0) wpart[warp][hq] = m2 > kFloor ? make_float2(m2 * kLn2, sm) : make_float2(-INFINITY, 0.f);
+        m_run[hq] = kFloor; s_run[hq] = 0.f;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");     // the 4 epilogue warps
       if (warp == 0 && lane < G) {
@@ -262,11 +270,17 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
     };
+    int bh = t_begin / tiles_per_head, tile = t_begin - bh * tiles_per_head;   // advanced incrementally
+    int cur_bh = bh;
+    float* lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
+    const int r = 32 * warp + lane;
     for (int i = 0; i < ntile; ++i) {
       const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
-      const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
-      if (bh != cur_bh) { flush(cur_bh); cur_bh = bh; }
-      const int b = bh / D.hk, h = bh - b * D.hk;
+      if (bh != cur_bh) {
+        flush(cur_bh);
+        cur_bh = bh;
+        lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
+      }
       mbar_wait(&acc_full[buf], aph);
       tc_fence_after();
       float v[16];
@@ -274,20 +288,25 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
-      const int r = 32 * warp + lane, j = tile * kSTile + r;
+      const int j = tile * kSTile + r;
       const bool out = (obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u;
+      if (warp == 0 && lane == 0 && i < 4) trace_tc_any(trace_buf, 8 + i);   // epilogue got tile i
       if (j < D.n_c) {
-        float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c + j;
 #pragma unroll
         for (int hq = 0; hq < G; ++hq) {
           const float x = out ? -INFINITY : v[hq] * scale;
-          lb[(size_t)hq * D.n_c] = x;
-          if (x > m_run[hq]) { s_run[hq] = s_run[hq] * expf(m_run[hq] - x) + 1.f; m_run[hq] = x; }
-          else if (x > -INFINITY) s_run[hq] += expf(x - m_run[hq]);
+          lrow[(size_t)hq * D.n_c + j] = x;
+          const float x2 = out ? kFloor : x * kLog2e;
+          const float mn = fmaxf(m_run[hq], x2);
+          s_run[hq] = fmaf(s_run[hq], exp2f(m_run[hq] - mn), out ? 0.f : exp2f(x2 - mn));
+          m_run[hq] = mn;
         }
       }
+      if (++tile == tiles_per_head) { tile = 0; ++bh; }
     }
+    if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 13);     // epilogue loop done
     flush(cur_bh);
+    if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 14);     // partials flushed
   }
   __syncthreads();
   trace_tc(trace_buf, 1);

@@ -16,6 +16,7 @@ from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace,
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--layers", type=int, default=4)
+ap.add_argument("--raw-epi", action="store_true", help="score events 8-11 hold clock64 deltas")
 ap.add_argument("--slots", type=int, default=1, help="trace this many consecutive layers (steady state)")
 args = ap.parse_args()
 os.environ["SKV_TRACE_SLOTS"] = str(args.slots)
@@ -62,7 +63,7 @@ if args.slots > 1:
               f"{col(2, 5, np.max):10.2f} {col(2, 7, np.max):10.2f}")
 t = T[args.slots - 1]
 t0 = t[0][t[0][:, 0] > 0][:, 0].min()
-names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "-", "-", "emitted", "nseg", "loaded_max", "exp_sum"],
+names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done", "epi_t0", "epi_t1", "epi_t2", "epi_t3", "mma0_issued", "epi_loop_done", "flushed"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "-", "-", "emitted", "nseg", "loaded_max", "exp_sum"],
          3: ["merge_start", "weights"],
          2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end", "pv_done", "synced"]}
 for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
@@ -75,3 +76,10 @@ for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
         if len(col):
             r = (col - t0) / 1e3
             print(f"   {en:14s} n={len(r):4d} min={r.min():8.2f} p50={np.median(r):8.2f} p90={np.percentile(r, 90):8.2f} max={r.max():8.2f} us")
+
+if args.raw_epi:
+    m = t[0][:148]
+    for e, nm in zip(range(8, 12), ["wait_acc_full", "tmem_ld", "arrive", "compute_store"]):
+        c = m[:, e]; c = c[c > 0]
+        if len(c):
+            print(f"   epi tile2 {nm:14s} cycles p50={np.median(c):8.0f} p90={np.percentile(c, 90):8.0f} max={c.max():8.0f}")
