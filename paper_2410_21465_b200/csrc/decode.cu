@@ -549,7 +549,7 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
   }
   trace(2, 6);
   __syncthreads();
-  if (!is_last) return;
+  if (!is_last) { trace(2, 10); return; }
   float* wsm = reinterpret_cast<float*>(scratch);          // [G][n_split] weights (A/B region is free)
   trace(3, 0);
   // o_hq = sum_s w_s o_s: thread = (split group sg of 8, float4 dims); the first batch of partial
@@ -636,6 +636,7 @@ __device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int b
     int* fl2 = flags + (size_t)bh * 4;
     fl2[0] = 0; fl2[1] = 0; fl2[2] = 0; fl2[3] = 0;
   }
+  trace(2, 10);
 }
 
 template <int G>

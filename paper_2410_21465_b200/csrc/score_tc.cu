@@ -149,6 +149,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     }
   }
   pdl_wait();                                          // everything below may read the caller's inputs
+  trace_tc(trace_buf, 15);
   if (ntile <= 0) return;
   const int nheads = (t_end - 1) / tiles_per_head - bh0 + 1;          // <= kTcMaxHeads (host check)
   // setup with every global load issued before any dependent use:
