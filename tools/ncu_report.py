@@ -64,6 +64,15 @@ def main(rep, out_md):
             traffic[f"{key}_dram_bytes"] = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
         except (ValueError, KeyError):
             pass
+        try:   # host-link bytes of the kernel (PCIe read rate x duration)
+            dur_s = val("gpu__time_duration.sum") * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(
+                units[hdr.index("gpu__time_duration.sum")], 1e-9)
+            i = hdr.index("pcie__read_bytes.sum.per_second")
+            pre = units[i].split("byte")[0]
+            rate = float(r[i].replace(",", "")) * {"": 1, "K": 1e3, "M": 1e6, "G": 1e9, "T": 1e12}.get(pre, 1)
+            traffic[f"{key}_pcie_read_bytes"] = rate * dur_s
+        except (ValueError, KeyError):
+            pass
     open(out_md, "w").write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out_md), "ncu_traffic.json")
     traffic["source"] = os.path.basename(rep)
