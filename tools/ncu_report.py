@@ -65,7 +65,7 @@ def main(rep, out_md):
         except (ValueError, KeyError):
             pass
         try:   # host-link bytes of the kernel (PCIe read rate x duration)
-            dur_s = val("gpu__time_duration.sum") * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(
+            dur_s = val("gpu__time_duration.sum") * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(
                 units[hdr.index("gpu__time_duration.sum")], 1e-9)
             i = hdr.index("pcie__read_bytes.sum.per_second")
             pre = units[i].split("byte")[0]
