@@ -371,9 +371,15 @@ def run_ours(args, cfg):
     host_bytes = b * cfg.n_kv_heads * cfg.budget * cfg.chunk * cfg.head_dim * 2          # HOST_alg per launch
     host_peak = measure_dma_h2d(pool)
     achieved = host_bytes / (g_avg_ms * 1e-3) / 1e9
-    traffic = load_ncu_traffic().get("sparse_attn_dram_bytes")
+    nt = load_ncu_traffic()
+    same = nt.get("config", "c2") == cfg.name and world == 1 and args.scaling == "weak"
+    traffic = nt.get("sparse_attn_dram_bytes") if same else None       # one ncu --set full capture, per launch
     roofline = {"bound": "host_link", "kernel": "k_sparse_attn", "achieved": achieved, "peak": host_peak,
                 "unit": "GB/s", "frac": achieved / host_peak, "traffic": traffic,
+                "traffic_pcie": nt.get("sparse_attn_pcie_read_bytes") if same else None,
+                "traffic_note": "traffic = dram__bytes_read+write of k_sparse_attn (A rows, B_h, outliers, window "
+                                "from HBM; algorithmic 7.1 MB at c2); traffic_pcie = its host-link reads "
+                                "(pcie__read_bytes, algorithmic 4.19 MB); source " + str(nt.get("source")),
                 "algorithmic_bytes_per_launch": host_bytes, "avg_launch_ms": g_avg_ms, "launches": g_cnt,
                 "share_of_step": g_ms / (prof_pass_ms * args.steps), "timing_pass_ms_per_step": prof_pass_ms,
                 "step_frac_of_roofline": (Lm * host_bytes / (host_peak * 1e9)) / (ms * 1e-3),

@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report (raw page) into markdown + the traffic JSON bench.py reads.
 
-python tools/ncu_report.py gpurun_out/<tag>_prof.ncu-rep profiles/<tag>_ncu_summary.md"""
+python tools/ncu_report.py gpurun_out/<tag>_prof.ncu-rep profiles/<tag>_ncu_summary.md [config, default c2]"""
 import csv
 import io
 import json
@@ -24,7 +24,7 @@ METRICS = [
 ]
 
 
-def main(rep, out_md):
+def main(rep, out_md, config="c2"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -76,9 +76,10 @@ def main(rep, out_md):
     open(out_md, "w").write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out_md), "ncu_traffic.json")
     traffic["source"] = os.path.basename(rep)
+    traffic["config"] = config
     json.dump(traffic, open(tj, "w"), indent=1)
     print(open(out_md).read())
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "c2")
