@@ -117,6 +117,18 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Split cluster barrier.  A release-arrive waits until this thread's earlier global stores are
+// performed, which on an SM with PCIe reads in flight can take tens of microseconds: arrive before
+// issuing global stores (or with .relaxed when only smem lifetime is at stake), wait after them.
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // address of the same smem variable in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
   uint32_t r; asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank)); return r;
@@ -135,6 +147,13 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
+// release-ordered fetch-add (orders this thread's earlier writes, and those made visible to it by
+// a CTA barrier, before the add: cumulativity) / acquire fence for the thread that observes it
+__device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
+  int old; asm volatile("atom.add.release.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // relaxed (coherent at gpu scope, unordered): for values that are their own payload, e.g. a
 // published chunk id that a consumer polls for
 __device__ __forceinline__ int ld_relaxed_gpu(const int* p) {

@@ -25,7 +25,6 @@
 
 namespace skv {
 
-constexpr int kMergeHeads = 4;         // heads whose partial loads are in flight together
 
 
 // optional per-CTA timeline (globaltimer ns) for tuning: [kernel][block < 4096][event < 16]
@@ -362,8 +361,8 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   const int rounds = (len + NT - 1) / NT;
   const bool prepub = !(B == 255 || n_per > 16384 || force_fb == 1);  // else: radix fallback publishes all k
   bool fallback = !prepub;
-  if (prepub) {
-    int wdef = 0;                                         // pass 1: candidates + definite count
+  int wdef = 0;
+  if (prepub) {                                           // pass 1: candidates + definite count
     for (int rd = 0; rd < rounds; ++rd) {
       const int j = rd * NT + tid;
       int bk = 256;
@@ -387,6 +386,10 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
     if (lane == 0) wdefs[warp] = wdef;
     __syncthreads();
+  }
+  // #2 (candidates published in smem): arrive now, wait after the slot stores below
+  cluster_arrive_release();
+  if (prepub) {
     if (wdef) {                                           // pass 2 (warp-uniform): publish
       int base = 0;                                       // lane w sums warp w's share, then reduce
       if (lane < NW) {
@@ -406,7 +409,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
   }
   trace(1, 5);
-  cluster_sync_all();                                                   // #2 candidates published
+  cluster_wait_acquire();                                               // #2 candidates visible
   trace(1, 6);
   int rc[kSelCL], total = 0, cmax = 0, off = 0;
 #pragma unroll
@@ -426,6 +429,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       akey[t] = (uint32_t)ld_dsmem_i32(dsmem_addr(&ckey[c], r));
     }
     __syncthreads();
+    cluster_arrive_relaxed();                            // #3: this CTA's DSMEM reads are done
     trace(1, 8);
     for (int t = off + tid; t < off + rc[crank]; t += NT) {
       const uint32_t u = akey[t];
@@ -481,7 +485,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       }
     }
     trace(1, 12);
-    cluster_sync_all();                                                 // #3 DSMEM reads finished
+    cluster_wait_acquire();                              // #3: peers done reading this CTA's smem
   } else {                   // pathological score distribution: exact radix select on one CTA
     float* zg = zws + bh * n;
     if (ZSMEM)
@@ -528,115 +532,76 @@ __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
   return s;
 }
 
-// The last unit of a (b, h) to finish merges all partials (log-sum-exp) into out, then leaves the
-// counter and flags zeroed for the next call.  A function (not a shared label) so that both exits
-// of k_sparse_attn reach the CTA barriers below through structured control flow.
+// a6 combine: out_hq = sum_s w_s o_s with w_s = exp(m_s - M) / sum_s' l_s' exp(m_s' - M) over the
+// per-unit partials (m_s, l_s, o_s) of one q head (split-KV log-sum-exp merge, fixed order).  A grid
+// of its own (one CTA per (b, hq), thread = dim) behind the relay grid: the kernel boundary orders
+// the partials before it (no fence in the sparse units, whose __threadfence stalls for tens of
+// microseconds while PCIe reads are in flight), and its griddepcontrol.wait is released ~0.8 us
+// after the sparse grid drains.  The first CTA of each (b, h) re-zeroes that head's slots and flags.
 template <int G>
-__device__ __forceinline__ void sparse_finish(const Dims& D, int b, int h, int bh, int n_split,
-                                              int* __restrict__ counters, int* __restrict__ flags,
-                                              int32_t* __restrict__ slots, const float* __restrict__ o_part, const float2* __restrict__ ml_part,
-                                              uint8_t* scratch, uint16_t* __restrict__ out) {
+__global__ void __launch_bounds__(kHeadDim)
+k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_part, int n_split,
+        int32_t* __restrict__ sel, int* __restrict__ flags, uint16_t* __restrict__ out, int late_trigger) {
   TRACE_INIT;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // ---- the last unit of this (b, h) to finish merges all partials (log-sum-exp) -> out
-  __shared__ int is_last;
-  __syncthreads();                                     // all partial stores of this CTA issued
-  trace(2, 9);
-  if (tid == 0) {
-    __threadfence();                                   // cumulative release of the CTA's partials
-    is_last = atomicAdd(&counters[bh], 1) == n_split - 1;
-    if (is_last) __threadfence();                      // acquire the other units' partials
-  }
-  trace(2, 6);
-  __syncthreads();
-  if (!is_last) { trace(2, 10); return; }
-  float* wsm = reinterpret_cast<float*>(scratch);          // [G][n_split] weights (A/B region is free)
+  extern __shared__ __align__(16) float2 mls[];          // [n_split]
+  const int row = blockIdx.x, d = threadIdx.x;            // row = b * hq + hq
+  if (!late_trigger) pdl_trigger();
+  pdl_wait();
   trace(3, 0);
-  // o_hq = sum_s w_s o_s: thread = (split group sg of 8, float4 dims); the first batch of partial
-  // loads is issued before the weights are known (independent), so the two L2 trips overlap
-  const int d4 = (tid & 31) * 4, sg = tid >> 5;
-  const int nper = (n_split - sg + 7) / 8;                      // splits of this group
-  auto load_batch = [&](int h0, int u0, float4 (&vv)[kMergeHeads][4]) {
+  const float2* mr = ml_part + (size_t)row * n_split;
+  const float* orow = o_part + (size_t)row * n_split * kHeadDim + d;
+  for (int i = d; i < n_split; i += kHeadDim) mls[i] = __ldcg(&mr[i]);
+  constexpr int kBatch = 64;                              // partial loads in flight per thread
+  float v[kBatch];
 #pragma unroll
-    for (int x = 0; x < kMergeHeads; ++x) {
-      const size_t row = (size_t)b * D.hq + (size_t)h * G + h0 + x;
-      const float4* opr = reinterpret_cast<const float4*>(o_part + row * n_split * kHeadDim + d4);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s2 = sg + 8 * (u0 + u);
-        vv[x][u] = (u0 + u < nper && h0 + x < G) ? __ldcg(opr + (size_t)s2 * (kHeadDim / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-  };
-  float4 vfirst[kMergeHeads][4];
-  load_batch(0, 0, vfirst);
-  // weights w_s = exp(m_s - M) / sum_s' l_s' exp(m_s' - M) per head, from the (m, l) partials
-  float2* mls = reinterpret_cast<float2*>(wsm + ((G * n_split + 3) & ~3) + kMergeHeads * 8 * kHeadDim);
-  const float2* mlb = ml_part + ((size_t)b * D.hq + (size_t)h * G) * n_split;
-  for (int i = tid; i < G * n_split; i += 256) mls[i] = __ldcg(&mlb[i]);
+  for (int u = 0; u < kBatch; ++u) v[u] = u < n_split ? __ldcg(orow + (size_t)u * kHeadDim) : 0.f;
+  // weights, computed once per CTA: M = max_s m_s; w_s = exp(m_s - M); L = sum_s l_s w_s
+  __shared__ float red[kHeadDim / 32];
+  float* w = reinterpret_cast<float*>(mls + n_split);     // [n_split]
+  const int lane = d & 31, warp = d >> 5;
   __syncthreads();
-  for (int hq = warp; hq < G; hq += 8) {
-    const float2* mr = mls + hq * n_split;
-    float M = -INFINITY;
-    for (int s2 = lane; s2 < n_split; s2 += 32) M = fmaxf(M, mr[s2].x);
-    M = warp_max(M);
-    float Ls = 0.f;
-    for (int s2 = lane; s2 < n_split; s2 += 32) { const float2 v = mr[s2]; if (v.x > -INFINITY) Ls = fmaf(v.y, expf(v.x - M), Ls); }
-    const float inv = 1.f / warp_sum(Ls);
-    for (int s2 = lane; s2 < n_split; s2 += 32) {
-      const float mx = mr[s2].x;
-      wsm[hq * n_split + s2] = mx > -INFINITY ? expf(mx - M) * inv : 0.f;
-    }
+  float mx = -INFINITY;
+  for (int s2 = d; s2 < n_split; s2 += kHeadDim) mx = fmaxf(mx, mls[s2].x);
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  float M = red[0];
+#pragma unroll
+  for (int i = 1; i < kHeadDim / 32; ++i) M = fmaxf(M, red[i]);
+  float Lp = 0.f;
+  for (int s2 = d; s2 < n_split; s2 += kHeadDim) {
+    const float2 ml = mls[s2];
+    const float ws = ml.x > -INFINITY ? expf(ml.x - M) : 0.f;
+    w[s2] = ws;
+    Lp = fmaf(ml.y, ws, Lp);
   }
+  Lp = warp_sum(Lp);
+  __syncthreads();                                        // w[] complete; red[] reads done
+  if (lane == 0) red[warp] = Lp;
   __syncthreads();
+  float L = 0.f;
+#pragma unroll
+  for (int i = 0; i < kHeadDim / 32; ++i) L += red[i];    // fixed order: deterministic
+  float acc = 0.f;
+  for (int s0 = 0; s0 < n_split; s0 += kBatch) {
+    if (s0 > 0) {
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) v[u] = s0 + u < n_split ? __ldcg(orow + (size_t)(s0 + u) * kHeadDim) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (s0 + u < n_split) acc = fmaf(w[s0 + u], v[u], acc);
+  }
+  if (late_trigger) pdl_trigger();                        // the next grid's prefetch after our loads
+  out[(size_t)row * kHeadDim + d] = f2bf(acc / L);
   trace(3, 1);
-  float* red = wsm + ((G * n_split + 3) & ~3);                  // [kMergeHeads][8][128]
-#pragma unroll
-  for (int h0 = 0; h0 < G; h0 += kMergeHeads) {
-    float4 a[kMergeHeads];
-#pragma unroll
-    for (int x = 0; x < kMergeHeads; ++x) a[x] = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto fma_batch = [&](int u0, const float4 (&vv)[kMergeHeads][4]) {
-#pragma unroll
-      for (int x = 0; x < kMergeHeads; ++x)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int s2 = sg + 8 * (u0 + u);
-          const float w = (u0 + u < nper && h0 + x < G) ? wsm[(h0 + x) * n_split + s2] : 0.f;
-          a[x].x = fmaf(w, vv[x][u].x, a[x].x); a[x].y = fmaf(w, vv[x][u].y, a[x].y);
-          a[x].z = fmaf(w, vv[x][u].z, a[x].z); a[x].w = fmaf(w, vv[x][u].w, a[x].w);
-        }
-    };
-    int u0 = 0;
-    if (h0 == 0) { fma_batch(0, vfirst); u0 = 4; }
-    for (; u0 < nper; u0 += 4) {
-      float4 vv[kMergeHeads][4];
-      load_batch(h0, u0, vv);
-      fma_batch(u0, vv);
-    }
-#pragma unroll
-    for (int x = 0; x < kMergeHeads; ++x)
-      if (h0 + x < G) *reinterpret_cast<float4*>(red + (x * 8 + sg) * kHeadDim + d4) = a[x];
-    __syncthreads();
-    for (int i = tid; i < kMergeHeads * kHeadDim; i += 256) {
-      const int x = i / kHeadDim, dd = i - x * kHeadDim;
-      if (h0 + x < G) {
-        float o = 0.f;
-#pragma unroll
-        for (int g2 = 0; g2 < 8; ++g2) o += red[(x * 8 + g2) * kHeadDim + dd];
-        out[((size_t)b * D.hq + (size_t)h * G + h0 + x) * kHeadDim + dd] = f2bf(o);
-      }
-    }
-    __syncthreads();
+  const int hq = row % D.hq;
+  if (hq % G == 0) {                                      // one CTA per (b, h): reset for the next call
+    const int bh = (row / D.hq) * D.hk + hq / G;
+    int32_t* slots = sel + (size_t)bh * D.k;
+    for (int i = d; i < D.k; i += kHeadDim) slots[i] = 0;
+    if (d < 4) flags[(size_t)bh * 4 + d] = 0;
   }
-  trace(2, 7);
-  for (int i = tid; i < D.k; i += 256) slots[i] = 0;    // leave slots, counter and flags zeroed
-  if (tid == 0) {                                         // for the next call
-    counters[bh] = 0;
-    int* fl2 = flags + (size_t)bh * 4;
-    fl2[0] = 0; fl2[1] = 0; fl2[2] = 0; fl2[3] = 0;
-  }
-  trace(2, 10);
 }
 
 template <int G>
@@ -644,8 +609,7 @@ __global__ void __launch_bounds__(256, 2)
 k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t* __restrict__ sel,
               int* __restrict__ flags, int step,
               float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
-              int n_split, float scale, uint16_t* __restrict__ dbg, int* __restrict__ counters,
-              uint16_t* __restrict__ out, int early_next) {
+              int n_split, float scale, uint16_t* __restrict__ dbg, int early_next) {
   TRACE_INIT;
   extern __shared__ __align__(128) uint8_t smem[];
   const AttnSmem lay = attn_smem_layout(D.r, G);
@@ -887,7 +851,6 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     }
   }
   trace(2, 8);
-  sparse_finish<G>(D, b, h, bh, n_split, counters, flags, slots, o_part, ml_part, smem + lay.a, out);
 }
 
 // =============================================================================================
@@ -941,6 +904,13 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Relay grid after k_sparse_attn (no body, no griddepcontrol.wait).  Measured
+// (tools/probe_pdl.cu): when a grid reads host-mapped memory, a PDL dependent that waits on it
+// directly is released ~4.5 us after its last CTA exits, against ~0.8 us otherwise.  With this
+// grid in between, the next kernel's griddepcontrol.wait still orders it after k_sparse_attn
+// (stream order) but is released ~0.8 us after it, i.e. 3.7 us earlier per layer.
+__global__ void k_relay() { pdl_trigger(); }
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -977,12 +947,6 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   }
   const int tph = ws.n_sblk;
   const int total_tiles = D.b * D.hk * tph;
-  {
-    const int nsu = (D.k + 7) / 8, nou = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
-    const int nsp = nsu + nou + (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
-    if ((size_t)(G * nsp + 4 + 8 * kMergeHeads * kHeadDim) * 4 + (size_t)G * nsp * 8 > (size_t)(lay.q - lay.a))
-      return cudaErrorInvalidConfiguration;                                           // merge scratch
-  }
   int grid_s = total_tiles < 2 * num_sms() ? total_tiles : 2 * num_sms();
   while (grid_s > 1 && (long long)tph * grid_s / total_tiles + 2 > kSegMax) --grid_s;   // select's slots
   // a1: tcgen05 score (TMA + TMEM); CUDA-core fallback when tensor maps are unavailable
@@ -1028,9 +992,21 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   const int early_next = (stg && stg[0] == '0') ? 0 : 1;
   if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
                       ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
-                      n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, ws.counters, out, early_next))) return e;
+                      n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, early_next))) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
-  *launches += 3;
+  const char* rl = getenv("SKV_NO_RELAY");              // tuning hook: 1 = omit the relay grid
+  if (!(rl && rl[0] == '1')) {
+    if ((e = launch_pdl(k_relay, dim3(1), dim3(32), 0, st))) return e;
+    *launches += 1;
+  }
+  const char* ml = getenv("SKV_MERGE_TRIGGER");        // tuning hook: late = after the partial loads
+  const int merge_late = (ml && ml[0] == 'l') ? 1 : 0;
+  if (prof) profile_mark(prof, kCombine, false, st);
+  if ((e = launch_pdl(k_merge<G>, dim3(D.b * D.hq), dim3(kHeadDim), (size_t)n_split * (sizeof(float2) + sizeof(float)), st, D,
+                      (const float*)ws.o_part, (const float2*)ws.ml_part, n_split, ws.sel, ws.flags, out,
+                      merge_late))) return e;
+  if (prof) profile_mark(prof, kCombine, true, st);
+  *launches += 4;
   return cudaGetLastError();
 }
 

@@ -19,6 +19,21 @@ __global__ void Dk(uint64_t* ts) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) atomicMin((unsigned long long*)&ts[1], (unsigned long long)gt());
 }
+// middle grid: no griddepcontrol.wait, busy for spin_ns, stamps its exit
+__global__ void M(uint64_t* ts, int spin_ns) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  uint64_t t0 = gt();
+  while (gt() - t0 < (uint64_t)spin_ns) {}
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax((unsigned long long*)&ts[3], (unsigned long long)gt());
+}
+static void launch_pdl_grid(void (*k)(uint64_t*), uint64_t* ts, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148); cfg.blockDim = dim3(128); cfg.stream = st;
+  cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1; cfg.attrs = at; cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, ts);
+}
 int main() {
   uint64_t* ts; cudaMalloc(&ts, 64);
   cudaStream_t st; cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -41,5 +56,24 @@ int main() {
         printf("host=%d P grid=%4d trigger=%d: D first CTA start %+8.2f us, D wait released %+6.2f us after P's last exit\n",
                host, grid, trig, ((double)h[2] - (double)h[0]) / 1e3, ((double)h[1] - (double)h[0]) / 1e3);
       }
+  printf("--- P (host reads, trigger) -> M (no wait, busy S us) -> D (wait)\n");
+  for (int spin : {0, 2000, 4000, 6000})
+    for (int rep = 0; rep < 2; ++rep) {
+      uint64_t init[4] = {0, ~0ull, ~0ull, 0};
+      cudaMemcpy(ts, init, 32, cudaMemcpyHostToDevice);
+      P<<<312, 256, 0, st>>>(ts, 20000, 1, dbuf, sink);
+      {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(8); cfg.blockDim = dim3(128); cfg.stream = st;
+        cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1; cfg.attrs = at; cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, M, ts, spin);
+      }
+      launch_pdl_grid(Dk, ts, st);
+      cudaStreamSynchronize(st);
+      uint64_t h[4]; cudaMemcpy(h, ts, 32, cudaMemcpyDeviceToHost);
+      printf("M busy %d ns: M exit %+6.2f us after P exit; D released %+6.2f us after P exit (%+6.2f after M exit)\n",
+             spin, ((double)h[3] - (double)h[0]) / 1e3, ((double)h[1] - (double)h[0]) / 1e3, ((double)h[1] - (double)h[3]) / 1e3);
+    }
   return 0;
 }

@@ -52,7 +52,7 @@ T = tr.view(args.slots, 4, 4096, 16).cpu().numpy().astype(np.float64)
 g0 = T[0, 0][T[0, 0][:, 0] > 0][:, 0].min()
 if args.slots > 1:
     print("== per-layer milestones (us from the first traced layer's score start)")
-    print("   layer  score_start pdl_rel  score_end  sel_start  pub(cand)  first_issue  p50_issue  last_V_in  merge_end  last_exit")
+    print("   layer  score_start pdl_rel  score_end  sel_start  pub(cand)  first_issue  p50_issue  last_V_in  merge_end  last_sparse_done")
     for sl in range(args.slots):
         t = T[sl]
         def col(k, e, f):
@@ -60,11 +60,11 @@ if args.slots > 1:
             return f(c - g0) / 1e3 if len(c) else float("nan")
         print(f"   {sl:5d}  {col(0, 0, np.min):10.2f} {col(0, 15, np.min):8.2f} {col(0, 1, np.max):9.2f} {col(1, 0, np.min):10.2f} "
               f"{col(1, 5, np.max):10.2f} {col(2, 2, np.min):11.2f} {col(2, 2, np.median):10.2f} "
-              f"{col(2, 5, np.max):10.2f} {col(2, 7, np.max):10.2f} {col(2, 10, np.max):10.2f}")
+              f"{col(2, 5, np.max):10.2f} {col(3, 1, np.max):10.2f} {col(2, 8, np.max):10.2f}")
 t = T[args.slots - 1]
 t0 = t[0][t[0][:, 0] > 0][:, 0].min()
 names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done", "epi_t0", "epi_t1", "epi_t2", "epi_t3", "mma0_issued", "epi_loop_done", "flushed", "pdl_released"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "-", "-", "emitted", "nseg", "loaded_max", "exp_sum"],
-         3: ["merge_start", "weights"],
+         3: ["merge_start", "merge_done"],
          2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end", "pv_done", "synced", "exit"]}
 for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
     m = t[kid]
