@@ -277,7 +277,14 @@ def run_ours(args, cfg):
         raise SystemExit(f"{per_layer * 2 * n_states / 1e9:.1f} GB of pinned values exceed host RAM; "
                          f"use a smaller --layer-states")
     t_setup = time.perf_counter()
-    pool = pinned_pool(per_layer * 2 * n_states)
+    while True:                 # page-locking can fail below the RAM estimate: fewer states then
+        try:
+            pool = pinned_pool(per_layer * 2 * n_states)
+            break
+        except RuntimeError:
+            if args.layer_states or n_states == 1:
+                raise
+            n_states = max(1, n_states // 2)
     states = []
     for l in range(n_states):
         inp = synth.gen_layer(cfg, seed, layer=l, device=dev)

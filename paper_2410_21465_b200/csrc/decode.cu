@@ -239,7 +239,7 @@ __device__ __forceinline__ int block_sum(int x, int* wsum) {
 }
 
 template <int G, bool ZSMEM>
-__global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 1)
+__global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 2)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
          int score_total, int score_grid, float* __restrict__ zws, int32_t* __restrict__ sel,
          int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int early_trigger,

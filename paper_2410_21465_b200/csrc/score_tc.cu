@@ -148,13 +148,21 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       tma_load_2d(sA + i * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[i]);
     }
   }
+  if (ntile <= 0) { pdl_wait(); return; }
+  const int nheads = (t_end - 1) / tiles_per_head - bh0 + 1;          // <= kTcMaxHeads (host check)
+  // outlier bitmap of this CTA's landmark rows (R3): layer state, built before the PDL wait
+  const int row_begin = t_begin * kSTile;
+  for (int w = tid; w < ntile * (kSTile / 32); w += kTcThreads) obits[w] = 0u;
+  __syncthreads();
+  for (int i = tid; i < nheads * D.o; i += kTcThreads) {
+    const int bh = bh0 + i / D.o, j = oids[(size_t)bh * D.o + i % D.o];
+    const int tr = bh * tiles_per_head * kSTile + j - row_begin;      // row in this CTA's tile space
+    if (tr >= 0 && tr < ntile * kSTile) atomicOr(&obits[tr >> 5], 1u << (tr & 31));
+  }
   pdl_wait();                                          // everything below may read the caller's inputs
   trace_tc(trace_buf, 15);
-  if (ntile <= 0) return;
-  const int nheads = (t_end - 1) / tiles_per_head - bh0 + 1;          // <= kTcMaxHeads (host check)
-  // setup with every global load issued before any dependent use:
-  //   B operands (q of each KV head in range, K-major SWIZZLE_128B, rows n >= G zero),
-  //   outlier bitmap of this CTA's landmark rows (R3), a7 window append (R18)
+  // B operands (q of each KV head in range, K-major SWIZZLE_128B, rows n >= G zero) and the a7
+  // window append (R18): call inputs, after the wait
   constexpr int kBChunks = kTcMaxHeads * 16 * 16;
   uint4 qv[(kBChunks + kTcThreads - 1) / kTcThreads];
 #pragma unroll
@@ -167,10 +175,12 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       qv[u] = *reinterpret_cast<const uint4*>(q + ((size_t)b * D.hq + (size_t)h * G + n) * kHeadDim + ch * 8);
     }
   }
-  int oid = -1, obh = 0;
-  if (tid < nheads * D.o && D.o > 0) { obh = bh0 + tid / D.o; oid = oids[(size_t)obh * D.o + tid % D.o]; }
-  const int row_begin = t_begin * kSTile;
-  for (int w = tid; w < ntile * (kSTile / 32); w += kTcThreads) obits[w] = 0u;
+  for (int idx = blockIdx.x * kTcThreads + tid; idx < D.b * D.hk * 32; idx += gridDim.x * kTcThreads) {
+    const int bh = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;
+    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + step) * kHeadDim + p * 8;
+    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bh * kHeadDim + p * 8;
+    *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
+  }
 #pragma unroll
   for (int u = 0; u < (kBChunks + kTcThreads - 1) / kTcThreads; ++u) {
     const int i = tid + u * kTcThreads;
@@ -180,23 +190,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       *reinterpret_cast<uint4*>(sB + hi * kBBytes + sub * 2048 + n * 128 + ((c16 ^ (n & 7)) << 4)) = qv[u];
     }
   }
-  for (int idx = blockIdx.x * kTcThreads + tid; idx < D.b * D.hk * 32; idx += gridDim.x * kTcThreads) {
-    const int bh = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;
-    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + step) * kHeadDim + p * 8;
-    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bh * kHeadDim + p * 8;
-    *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
-  }
   trace_tc(trace_buf, 6);
-  __syncthreads();
-  if (oid >= 0) {
-    const int tr = obh * tiles_per_head * kSTile + oid - row_begin;   // row in this CTA's tile space
-    if (tr >= 0 && tr < ntile * kSTile) atomicOr(&obits[tr >> 5], 1u << (tr & 31));
-  }
-  for (int i = kTcThreads + tid; i < nheads * D.o; i += kTcThreads) {    // (o > 48 per head: rare)
-    const int bh = bh0 + i / D.o, j = oids[(size_t)bh * D.o + i % D.o];
-    const int tr = bh * tiles_per_head * kSTile + j - row_begin;
-    if (tr >= 0 && tr < ntile * kSTile) atomicOr(&obits[tr >> 5], 1u << (tr & 31));
-  }
   fence_proxy_async();                                    // B (generic writes) -> UMMA (async proxy)
   tc_fence_before();
   __syncthreads();
