@@ -138,6 +138,9 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank)
 __device__ __forceinline__ int ld_dsmem_i32(uint32_t a) {
   int v; asm("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a)); return v;
 }
+__device__ __forceinline__ void st_dsmem_i32(uint32_t a, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t a) {
   float v; asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v;
 }

@@ -249,13 +249,13 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   extern __shared__ __align__(16) float zdyn[];
   __shared__ TopKSmem<NT> tk;
   __shared__ float lse[G], hm[G];
-  __shared__ int hist[256], ghist[256], below[kSelCL], info[4], wdefs[NT / 32];
+  __shared__ int hist[256], ghist[256], below[kSelCL], info[4];
+  __shared__ int allhist[kSelCL * 256];                 // every rank's histogram (pushed before #1)
   __shared__ int cidx[kSelCandLocal], ccnt;
   __shared__ uint32_t ckey[kSelCandLocal];
   __shared__ int aidx[kSelCandLocal];
   __shared__ uint32_t akey[kSelCandLocal];
   __shared__ int tks[kSelCandLocal], tkf[kSelCandLocal];
-  __shared__ int wtmp[NW * kSelCL], wcnt[NW * 64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t crank = cluster_ctarank();
   const size_t bh = blockIdx.x / kSelCL;
@@ -319,17 +319,22 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       }
     }
   }
+  __syncthreads();                                                      // local histogram complete
+  // push this rank's histogram into allhist[crank][.] of every rank (the release-arrive of barrier #1
+  // orders these remote stores), so that after the barrier all histograms are local reads
+  if (tid < 256) {
+    const int v = hist[tid];
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r) st_dsmem_i32(dsmem_addr(&allhist[crank * 256 + tid], r), v);
+  }
   trace(1, 3);
   cluster_sync_all();                                                   // #1 histograms published
   trace(1, 4);
-  if (!early_trigger) pdl_trigger();                    // sparse CTAs launch and wait on the flags below
-  int hv[kSelCL];                                       // thread i < 256 owns bin i of every rank
-#pragma unroll
-  for (int r = 0; r < kSelCL; ++r) hv[r] = tid < 256 ? ld_dsmem_i32(dsmem_addr(&hist[tid], r)) : 0;
+  if (!early_trigger) pdl_trigger();                    // sparse CTAs launch and poll their slots
   if (tid < 256) {
     int g = 0;
 #pragma unroll
-    for (int r = 0; r < kSelCL; ++r) g += hv[r];
+    for (int r = 0; r < kSelCL; ++r) g += allhist[r * 256 + tid];
     ghist[tid] = g;
   }
   __syncthreads();
@@ -351,61 +356,54 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
   }
   __syncthreads();
+  trace(1, 10);
   const int B = info[0], need = info[1];
-  // The selection is published UNORDERED into k slots (chunk id + 1; 0 = not yet): attention is a
-  // sum over the selected set, so no prefix scan has to run before a value fetch can start.  The
-  // chunks strictly above the threshold bucket ("definite") take slots [0, k - need) through one
-  // atomic reservation per warp right away; the `need` winners of the threshold bucket take
-  // [k - need, k) once ranked.  Each sparse-attention unit polls its own 8 slots.
+  if (warp < kSelCL) {                                  // below[r]: rank r's histogram mass above B
+    int sb = 0;
+    for (int bin = lane; bin < B; bin += 32) sb += allhist[warp * 256 + bin];
+    sb = __reduce_add_sync(0xffffffffu, sb);
+    if (lane == 0) below[warp] = sb;
+  }
+  // The selection is published into k slots (chunk id + 1; 0 = not yet) before it is complete:
+  // attention is a sum over the selected set, so the chunks strictly above the threshold bucket
+  // ("definite") are written to slots [0, k - need) as soon as B is known, and the `need` winners of
+  // bucket B fill [k - need, k) once ranked.  Positions are deterministic (rank prefix, then index
+  // order inside the rank), so the definite part is even ascending.  Each sparse-attention unit
+  // polls its own 8 slots.
   int32_t* slots = sel + bh * k;
-  const int rounds = (len + NT - 1) / NT;
   const bool prepub = !(B == 255 || n_per > 16384 || force_fb == 1);  // else: radix fallback publishes all k
   bool fallback = !prepub;
-  int wdef = 0;
-  if (prepub) {                                           // pass 1: candidates + definite count
-    for (int rd = 0; rd < rounds; ++rd) {
-      const int j = rd * NT + tid;
-      int bk = 256;
+  const int per = (len + NT - 1) / NT;                  // this thread's contiguous run [ja, jb)
+  const int ja = min(len, tid * per), jb = min(len, ja + per);
+  int ndef = 0;
+  if (prepub) {                                         // one pass: candidates of B, definite count
+    for (int i = 0; i < per; ++i) {                     // warp-uniform trip count (ballots inside)
+      const int j = ja + i;
       float zz = -INFINITY;
-      if (j < len) { zz = z[j]; if (zz > -INFINITY) bk = zbucket(zz, zmax); }
-      if (bk == B) {
-        const int pos = atomicAdd(&ccnt, 1);
-        if (pos < kSelCandLocal) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
+      int bk = 256;
+      if (j < jb) { zz = z[j]; if (zz > -INFINITY) bk = zbucket(zz, zmax); }
+      ndef += bk < B;
+      const unsigned cb = __ballot_sync(0xffffffffu, bk == B);
+      if (cb) {                                         // warp-aggregated slot reservation
+        int base = 0;
+        if (lane == __ffs(cb) - 1) base = atomicAdd(&ccnt, __popc(cb));
+        base = __shfl_sync(0xffffffffu, base, __ffs(cb) - 1);
+        const int pos = base + __popc(cb & ((1u << lane) - 1u));
+        if (bk == B && pos < kSelCandLocal) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
       }
-      const int c = __popc(__ballot_sync(0xffffffffu, bk < B));
-      if (lane == 0) wcnt[rd * NW + warp] = c;
-      wdef += c;
     }
-    // deterministic slot positions (the summation order of the output must not depend on timing):
-    // [ranks below this one][warps below this one][rounds][lanes].  A rank's definite count is its
-    // histogram mass above bucket B, summed from the per-rank histograms already in registers.
-#pragma unroll
-    for (int r = 0; r < kSelCL; ++r) {
-      const int v = __reduce_add_sync(0xffffffffu, tid < B ? hv[r] : 0);
-      if (lane == 0) wtmp[warp * kSelCL + r] = v;
-    }
-    if (lane == 0) wdefs[warp] = wdef;
-    __syncthreads();
   }
+  int dtot;
+  const int dex = block_exclusive_scan<NT>(ndef, tk, &dtot);          // (synchronises the CTA)
+  trace(1, 11);
   // #2 (candidates published in smem): arrive now, wait after the slot stores below
   cluster_arrive_release();
-  if (prepub) {
-    if (wdef) {                                           // pass 2 (warp-uniform): publish
-      int base = 0;                                       // lane w sums warp w's share, then reduce
-      if (lane < NW) {
-        base = lane < warp ? wdefs[lane] : 0;
-#pragma unroll
-        for (int r = 0; r < kSelCL; ++r) base += r < (int)crank ? wtmp[lane * kSelCL + r] : 0;
-      }
-      base = __reduce_add_sync(0xffffffffu, base);
-      for (int rd = 0; rd < rounds; ++rd) {
-        const int j = rd * NT + tid;
-        bool def = false;
-        if (j < len) { const float zz = z[j]; def = zz > -INFINITY && zbucket(zz, zmax) < B; }
-        const unsigned bal = __ballot_sync(0xffffffffu, def);
-        if (def) st_relaxed_gpu(&slots[base + __popc(bal & ((1u << lane) - 1u))], lo + j + 1);
-        base += __popc(bal);
-      }
+  if (ndef) {
+    int base = dex;
+    for (int r = 0; r < (int)crank; ++r) base += below[r];
+    for (int j = ja; j < jb; ++j) {
+      const float zz = z[j];
+      if (zz > -INFINITY && zbucket(zz, zmax) < B) st_relaxed_gpu(&slots[base++], lo + j + 1);
     }
   }
   trace(1, 5);
@@ -457,31 +455,24 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
         for (int c = 0; c < total; ++c) ord += tkf[c] && aidx[c] < j;
         tks[ord] = j;
       }
-      if (tid < kSelCL) { int t = 0; for (int w = 0; w < NW; ++w) t += wtmp[w * kSelCL + tid]; below[tid] = t; }
-      int tot;
-      const int mine = tid < rounds * NW ? wcnt[tid] : 0;
-      const int ex = block_exclusive_scan<NT>(mine, tk, &tot);      // (synchronises the CTA)
-      if (tid < rounds * NW) wcnt[tid] = ex;
       __syncthreads();
-      int base_def = 0;
-#pragma unroll
-      for (int r = 0; r < kSelCL; ++r) base_def += r < (int)crank ? below[r] : 0;
-      const int nt = need;
-      for (int rd = 0; rd < rounds; ++rd) {
-        const int j = rd * NT + tid;
-        bool def = false, taken = false;
-        if (j < len) {
-          const float zz = z[j];
-          taken = zz == INFINITY;
-          def = !taken && zz > -INFINITY && zbucket(zz, zmax) < B;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, def);
-        if (def || taken) {
-          const int jj = lo + j;
-          int lo2 = 0, hi2 = nt;                          // #taken with index < jj
-          while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < jj) lo2 = mid + 1; else hi2 = mid; }
-          sel_user[bh * k + base_def + wcnt[rd * NW + warp] + __popc(bal & ((1u << lane) - 1u)) + lo2] = jj;
-        }
+      int base_sel = 0;                                  // selected chunks of the ranks below
+      for (int r = 0; r < (int)crank; ++r) base_sel += below[r];
+      {
+        int lo2 = 0, hi2 = need;                         // + taken ones with index < lo
+        while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (tks[mid] < lo) lo2 = mid + 1; else hi2 = mid; }
+        base_sel += lo2;
+      }
+      int nsel = 0;
+      for (int j = ja; j < jb; ++j) {
+        const float zz = z[j];
+        nsel += zz == INFINITY || (zz > -INFINITY && zbucket(zz, zmax) < B);
+      }
+      int stot;
+      int pos = base_sel + block_exclusive_scan<NT>(nsel, tk, &stot);
+      for (int j = ja; j < jb; ++j) {
+        const float zz = z[j];
+        if (zz == INFINITY || (zz > -INFINITY && zbucket(zz, zmax) < B)) sel_user[bh * k + pos++] = lo + j;
       }
     }
     trace(1, 12);
