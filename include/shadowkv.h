@@ -127,7 +127,11 @@ SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *ro
  * out    device bf16 [b][h_q][d]
  * sel_ids   nullable device int32 [b][h_kv][k]  -- parity hook for a3
  * dbg_keys  nullable device bf16 [b][h_kv][k*c][d] -- parity hook for a4 (rebuilt, post-RoPE)
- * Requires window_cap >= w_eff + step + 1 (SKV_EINVAL otherwise). */
+ * Requires window_cap >= w_eff + step + 1 (SKV_EINVAL otherwise).
+ * Streams: all work is ordered after earlier work on `stream`, and later work on `stream` is
+ * ordered after all of it.  For batches of >= 32 requests the call pipelines request sub-batches:
+ * it forks part of the work onto internal high-priority streams (event fork/join, capture-safe)
+ * and joins them back into `stream` before returning (SKV_SPLIT=n overrides the sub-batch count). */
 SKV_API skv_status shadowkv_decode_step(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
                                 const uint16_t *q, const uint16_t *k_new, const uint16_t *v_new,
                                 int32_t step, uint16_t *out, int32_t *sel_ids, uint16_t *dbg_keys,

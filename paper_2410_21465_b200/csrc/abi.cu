@@ -86,9 +86,7 @@ skv_status check_layer(const skv_layer* l, const skv::Dims& D, skv::Layer* Ly) {
 }
 
 size_t ws_bytes(const skv::Dims& D) {
-  size_t a = skv::build_ws_bytes(D, nullptr, nullptr);
-  size_t b = skv::decode_ws_bytes(D, nullptr, nullptr);
-  return a > b ? a : b;
+  return skv::build_ws_bytes(D, nullptr, nullptr);   // build scratch sits after every decode region
 }
 
 }  // namespace
@@ -227,15 +225,13 @@ skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, cons
     return fail(SKV_EINVAL, "q/k_new/v_new/out/sel_ids/dbg_keys must be 16-byte aligned");
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
-  skv::DecodeWs ws;
-  skv::decode_ws_bytes(D, &ws, static_cast<char*>(workspace));
   if (g_trace_on) {          // consecutive calls stamp consecutive trace blocks (SKV_TRACE_SLOTS, default 1)
     const char* ns = getenv("SKV_TRACE_SLOTS");
     const int n = ns ? atoi(ns) : 1;
     D.trace_slot = n > 1 ? g_trace_calls++ % n : 0;
   }
   int launches = 0;
-  cudaError_t e = skv::launch_decode(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws,
+  cudaError_t e = skv::launch_decode(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, static_cast<char*>(workspace),
                                      static_cast<cudaStream_t>(stream), &launches, g_prof);
   if (e != cudaSuccess) return fail(SKV_ECUDA, "decode launch failed: %s", cudaGetErrorString(e));
   g_launches = launches;

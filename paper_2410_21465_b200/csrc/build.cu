@@ -105,7 +105,9 @@ k_build_outliers_window(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ K
 }
 
 size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base) {
-  size_t off = ws_header_bytes(D);                  // never touch decode's counters
+  // after every decode region (all sub-batch splits): decode's counters, flags and selection slots
+  // must stay zero between calls, so the build scratch never overlaps them
+  size_t off = (decode_ws_total_bytes(D) + 255) & ~(size_t)255;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return base + o; };
   size_t n = (size_t)D.b * D.hk * D.n_c;
   char* p1 = carve(n * 4);

@@ -91,7 +91,8 @@ cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const ui
                          const BuildWs& ws, cudaStream_t st, int* launches);
 cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                           const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
-                          int32_t* sel_ids, uint16_t* dbg_keys, const DecodeWs& ws, cudaStream_t st,
+                          int32_t* sel_ids, uint16_t* dbg_keys, char* ws_base, cudaStream_t st,
                           int* launches, Profiler* prof);
+size_t decode_ws_total_bytes(const Dims& D);   // every sub-batch split's workspace fits
 
 }  // namespace skv
