@@ -269,7 +269,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   trace(1, 0);
   if (early_trigger) pdl_trigger();                     // sparse-attn CTAs may start their prologue
   for (int i = tid; i < 256; i += NT) hist[i] = 0;
-  if (tid == 0) { ccnt = 0; info[0] = info[1] = 0; }
+  if (tid == 0) { ccnt = 0; info[0] = 255; info[1] = 0; }   // B = 255 unless bins 0..254 reach k
   pdl_wait();
   trace(1, 1);
   int* fl = flags + bh * 4;
@@ -315,7 +315,10 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lg[u][hq] - lse[hq]);
       if (j < len) {
         z[j] = zz;
-        if (zz > -INFINITY) atomicAdd(&hist[zbucket(zz, zmax)], 1);
+        // the catch-all bucket 255 is never counted: if bins 0..254 hold fewer than k, B stays 255
+        // and the exact radix fallback runs
+        const int bk = zz > -INFINITY ? zbucket(zz, zmax) : 255;
+        if (bk != 255) atomicAdd(&hist[bk], 1);
       }
     }
   }
