@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k
   --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
 if [ "$2" == "full" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sparse_attn|k_score|k_select" -s 96 -c 3 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sparse_attn|k_score|k_select|k_merge" -s 128 -c 4 \
     -o gpurun_out/${TAG}_prof python bench.py --steps 2 --warmup 1 --e2e-steps 1 --no-cpu-baseline \
     > gpurun_out/${TAG}_ncu_full.log 2>&1
   echo "ncu full rc=$?"
