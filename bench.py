@@ -122,6 +122,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
+def bind_to_gpu_numa(local: int) -> str:
+    """Restrict this process to the CPUs NVML reports as local to its GPU, so that the pinned value
+    pool is first-touched (allocated) on that NUMA node and the host->GPU reads stay node-local."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        pr = torch.cuda.get_device_properties(local)        # NVML index != CUDA index under CUDA_VISIBLE_DEVICES
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus and cpus != set(range(os.cpu_count())):
+            os.sched_setaffinity(0, cpus)
+            return f"bound to {len(cpus)} GPU-local CPUs"
+        return "all CPUs GPU-local"
+    except Exception as e:                       # no NVML / no affinity info: leave it to the OS
+        return f"unbound ({type(e).__name__})"
+
+
 def pinned_pool(nbytes: int) -> torch.Tensor:
     """One page-locked, device-mapped host buffer (cudaHostRegister portable|mapped)."""
     buf = torch.empty(nbytes // 2, dtype=torch.bfloat16)
@@ -245,6 +264,7 @@ def run_reference(args, cfg):
 def run_ours(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    numa_note = bind_to_gpu_numa(local)          # before the pinned pool is first touched
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -408,7 +428,7 @@ def run_ours(args, cfg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/; random rank-160 factors)",
-            "config": dict(workload_config(cfg, world), layer_states=n_states),
+            "config": dict(workload_config(cfg, world), layer_states=n_states, host_numa=numa_note),
             "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
