@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="extra untimed pass timing every kernel")
+    ap.add_argument("--graph", choices=["on", "off"], default="on",
+                    help="time CUDA-graph replays of the 32-layer step (shadowkv_decode_step_dev, device-side step "
+                         "counter) instead of per-call stream launches")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: every rank runs the config's batch; strong: the batch is split over ranks")
     ap.add_argument("--layer-states", type=int, default=0,
@@ -338,6 +341,34 @@ def run_ours(args, cfg):
     for i in range(args.warmup):
         step(i, *dev_inputs[i])
     torch.cuda.synchronize()
+
+    # --- CUDA graph of one whole step: every layer through shadowkv_decode_step_dev (the step index
+    #     lives in device memory) + the counter increment; replays advance the decode step ------------
+    use_graph = args.graph == "on"
+    if use_graph:
+        q_g = torch.empty_like(dev_inputs[0][0]); k_g = torch.empty_like(dev_inputs[0][1])
+        v_g = torch.empty_like(dev_inputs[0][2])
+        step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        cap = torch.cuda.Stream()
+        graph_launches = [0]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            for l in range(Lm):
+                states[l % n_states].decode_dev(rope.struct, q_g[l], k_g[l], v_g[l], step_dev, n_total, out[l], ws,
+                                                stream=cap)
+                graph_launches[0] += bd.shadowkv_last_launch_count()
+            step_dev.add_(1)
+        step_dev.fill_(args.warmup)
+        torch.cuda.synchronize()
+
+    def run_step(i, q, kn, vn):
+        if use_graph:
+            q_g.copy_(q, non_blocking=True); k_g.copy_(kn, non_blocking=True); v_g.copy_(vn, non_blocking=True)
+            g.replay()
+            launches[0] += graph_launches[0]
+        else:
+            step(i, q, kn, vn)
+
     if world > 1:
         torch.distributed.barrier()
     launches[0] = 0
@@ -346,7 +377,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         e0.record(stream)
         for i in range(args.warmup, args.warmup + args.steps):
-            step(i, *dev_inputs[i])
+            run_step(i, *dev_inputs[i])
         e1.record(stream)
         torch.cuda.synchronize()
     gpu_launches = launches[0]
@@ -382,8 +413,12 @@ def run_ours(args, cfg):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for j, (qh, kh, vh) in enumerate(host_inputs):
-        q_d.copy_(qh, non_blocking=True); k_d.copy_(kh, non_blocking=True); v_d.copy_(vh, non_blocking=True)
-        step(i0 + j, q_d, k_d, v_d)
+        if use_graph:                                          # H2D straight into the graph's input buffers
+            q_g.copy_(qh, non_blocking=True); k_g.copy_(kh, non_blocking=True); v_g.copy_(vh, non_blocking=True)
+            g.replay()
+        else:
+            q_d.copy_(qh, non_blocking=True); k_d.copy_(kh, non_blocking=True); v_d.copy_(vh, non_blocking=True)
+            step(i0 + j, q_d, k_d, v_d)
         out_h.copy_(out, non_blocking=True)
         stream.synchronize()                                   # host reads the step's result
     f1.record(stream)
@@ -428,7 +463,9 @@ def run_ours(args, cfg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/; random rank-160 factors)",
-            "config": dict(workload_config(cfg, world), layer_states=n_states, host_numa=numa_note),
+            "config": dict(workload_config(cfg, world), layer_states=n_states, host_numa=numa_note,
+                           launch="one CUDA graph per 32-layer step (shadowkv_decode_step_dev)" if use_graph
+                           else "stream launches (shadowkv_decode_step)"),
             "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},

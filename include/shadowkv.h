@@ -137,6 +137,17 @@ SKV_API skv_status shadowkv_decode_step(const skv_dims *dims, const skv_rope *ro
                                 int32_t step, uint16_t *out, int32_t *sel_ids, uint16_t *dbg_keys,
                                 void *workspace, void *stream);
 
+/* Graph-replayable variant of shadowkv_decode_step: identical computation, but the step index is
+ * read on the device from *step_dev (int32, 4-byte aligned, device memory, written by work ordered
+ * before this call on `stream`, e.g. an increment captured in the same CUDA graph), so one captured
+ * graph serves every decode step.  Values are clamped to [0, max_step]; the launch is sized for
+ * max_step (window units past the live window contribute nothing).  Requires window_cap >= w_eff +
+ * max_step + 1.  Same buffers, streams and errors as shadowkv_decode_step. */
+SKV_API skv_status shadowkv_decode_step_dev(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
+                                    const uint16_t *q, const uint16_t *k_new, const uint16_t *v_new,
+                                    const int32_t *step_dev, int32_t max_step, uint16_t *out, int32_t *sel_ids,
+                                    uint16_t *dbg_keys, void *workspace, void *stream);
+
 /* Thread-local description of the last non-OK status ("" if none). */
 SKV_API const char *shadowkv_last_error(void);
 

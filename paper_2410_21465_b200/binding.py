@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libshadowkv.so")
 
 SKV_OK, SKV_EINVAL, SKV_EUNSUPPORTED, SKV_ECUDA, SKV_ESTATE = range(5)
 STATUS_NAMES = {0: "SKV_OK", 1: "SKV_EINVAL", 2: "SKV_EUNSUPPORTED", 3: "SKV_ECUDA", 4: "SKV_ESTATE"}
-EXPORTED = ["shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step",
+EXPORTED = ["shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step", "shadowkv_decode_step_dev",
             "shadowkv_last_error", "shadowkv_abi_version", "shadowkv_last_launch_count",
             "shadowkv_profile_begin", "shadowkv_profile_end", "shadowkv_trace_buffer"]
 KERNEL_NAMES = ["score", "select", "sparse_attn", "reserved", "combine"]
@@ -64,6 +64,10 @@ def load(path: str = LIB_PATH):
     lib.shadowkv_decode_step.argtypes = [P(SkvDims), P(SkvRope), P(SkvLayer), ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.shadowkv_decode_step_dev.restype = ctypes.c_int
+    lib.shadowkv_decode_step_dev.argtypes = [P(SkvDims), P(SkvRope), P(SkvLayer), ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     lib.shadowkv_last_error.restype = ctypes.c_char_p
     lib.shadowkv_last_error.argtypes = []
     lib.shadowkv_abi_version.restype = ctypes.c_int32
@@ -129,6 +133,13 @@ def shadowkv_decode_step(dims: SkvDims, rope: SkvRope, layer: SkvLayer, q, k_new
     _check(load().shadowkv_decode_step(ctypes.byref(dims), ctypes.byref(rope), ctypes.byref(layer), _ptr(q),
                                        _ptr(k_new), _ptr(v_new), int(step), _ptr(out), _ptr(sel_ids),
                                        _ptr(dbg_keys), _ptr(workspace), _stream_ptr(stream)))
+
+
+def shadowkv_decode_step_dev(dims: SkvDims, rope: SkvRope, layer: SkvLayer, q, k_new, v_new, step_dev,
+                             max_step: int, out, sel_ids=None, dbg_keys=None, workspace=None, stream=None):
+    _check(load().shadowkv_decode_step_dev(ctypes.byref(dims), ctypes.byref(rope), ctypes.byref(layer), _ptr(q),
+                                           _ptr(k_new), _ptr(v_new), _ptr(step_dev), int(max_step), _ptr(out),
+                                           _ptr(sel_ids), _ptr(dbg_keys), _ptr(workspace), _stream_ptr(stream)))
 
 
 def shadowkv_last_launch_count() -> int:

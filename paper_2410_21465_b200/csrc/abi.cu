@@ -56,7 +56,7 @@ skv_status check_dims(const skv_dims* d, skv::Dims* D) {
   if (d->window_cap < w_eff || d->window_cap < 1)
     return fail(SKV_EINVAL, "window_cap %d < w_eff %d", d->window_cap, w_eff);
   *D = skv::Dims{d->batch, d->n_q_heads, d->n_kv_heads, g, d->head_dim, d->ctx_len, d->rank, d->chunk,
-                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff, 0};
+                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff, 0, nullptr, 0};
   return SKV_OK;
 }
 
@@ -207,13 +207,18 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
   return SKV_OK;
 }
 
-skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
-                                const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
-                                int32_t step, uint16_t* out, int32_t* sel_ids, uint16_t* dbg_keys,
-                                void* workspace, void* stream) {
+static skv_status decode_impl(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
+                              const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                              int32_t step, const int32_t* step_dev, uint16_t* out, int32_t* sel_ids,
+                              uint16_t* dbg_keys, void* workspace, void* stream) {
   skv::Dims D; skv::Rope R; skv::Layer Ly;
   skv_status st;
   if ((st = check_dims(dims, &D)) != SKV_OK) return st;
+  if (step_dev) {
+    if (reinterpret_cast<uintptr_t>(step_dev) & 3u) return fail(SKV_EINVAL, "step_dev must be 4-byte aligned");
+    D.step_dev = step_dev;
+    D.max_step = step;                                   // step carries max_step for the device variant
+  }
   if ((st = check_rope(rope, D.d, &R)) != SKV_OK) return st;
   if ((st = check_layer(layer, D, &Ly)) != SKV_OK) return st;
   if (step < 0) return fail(SKV_EINVAL, "step must be >= 0");
@@ -237,6 +242,22 @@ skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, cons
   g_launches = launches;
   g_err.clear();
   return SKV_OK;
+}
+
+skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
+                                const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                                int32_t step, uint16_t* out, int32_t* sel_ids, uint16_t* dbg_keys,
+                                void* workspace, void* stream) {
+  return decode_impl(dims, rope, layer, q, k_new, v_new, step, nullptr, out, sel_ids, dbg_keys, workspace, stream);
+}
+
+skv_status shadowkv_decode_step_dev(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
+                                    const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                                    const int32_t* step_dev, int32_t max_step, uint16_t* out, int32_t* sel_ids,
+                                    uint16_t* dbg_keys, void* workspace, void* stream) {
+  if (!step_dev) return fail(SKV_EINVAL, "step_dev must be non-NULL");
+  return decode_impl(dims, rope, layer, q, k_new, v_new, max_step, step_dev, out, sel_ids, dbg_keys, workspace,
+                     stream);
 }
 
 }  // extern "C"

@@ -27,6 +27,14 @@ namespace skv {
 
 
 
+// the decode step: the launch argument, or the device counter of a graph-replayable call (written
+// by the caller's stream before this call, so read with acquire semantics), clamped to the range the
+// grid and the window were sized for
+__device__ __forceinline__ int cur_step(const Dims& D, int step) {
+  if (!D.step_dev) return step;
+  return min(max(ld_acquire_gpu(D.step_dev), 0), D.max_step);
+}
+
 // optional per-CTA timeline (globaltimer ns) for tuning: [kernel][block < 4096][event < 16]
 __device__ uint64_t* g_trace = nullptr;
 // kernels read g_trace once (TRACE_INIT) so that disabled tracing costs no dependent loads
@@ -118,9 +126,10 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
   trace(0, 0);
   pdl_trigger();                                       // let the select grid become resident early
   // a7: append the current token's K, V to the window (R18)
+  const int stp = cur_step(D, step);
   for (int idx = blockIdx.x * 256 + tid; idx < D.b * D.hk * 32; idx += gridDim.x * 256) {
     const int bh = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;
-    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + step) * kHeadDim + p * 8;
+    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + stp) * kHeadDim + p * 8;
     const uint16_t* src = (arr ? v_new : k_new) + (size_t)bh * kHeadDim + p * 8;
     *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
   }
@@ -618,7 +627,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane & 15;
   const int d = tid & 127, hh = tid >> 7;                      // PV / merge ownership: dim, head parity
   const int BH = D.b * D.hk;
-  const int T_out = D.o * kChunk, T_win = D.w_eff + step + 1;
+  const int T_out = D.o * kChunk, T_win = D.w_eff + cur_step(D, step) + 1;
   int u = blockIdx.x, kind, bh, ui;
   if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
   else {
@@ -760,6 +769,14 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       ntok = min(kUnitTok, T_win - ui * kUnitTok);
       Ksrc = Ly.K_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
       Vsrc = Ly.V_win + ((size_t)bh * D.wcap + ui * kUnitTok) * kHeadDim;
+    }
+    if (ntok <= 0) {                 // window unit past the live window (grid sized for max_step)
+      for (int hq = tid >> 7; hq < G; hq += 2) {
+        const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+        o_part[row * kHeadDim + (tid & 127)] = 0.f;
+        if ((tid & 127) == 0) ml_part[row] = make_float2(-INFINITY, 0.f);
+      }
+      return;
     }
     if (tid == 0) {
       mbar_expect_tx(&barAB, ntok * kHeadDim * 2);
@@ -991,7 +1008,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     if (ev_sel && (e = cudaEventRecord(ev_sel, st))) return e;   // sub-batch pipelining: next chain may start
   }
   const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
-  const int n_win_u = (D.w_eff + step + 1 + kUnitTok - 1) / kUnitTok;
+  const int n_win_u = (D.w_eff + (D.step_dev ? D.max_step : step) + 1 + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_u;
   const int units = D.b * D.hk * n_split;
   // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score

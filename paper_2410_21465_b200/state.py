@@ -92,6 +92,13 @@ class LayerState:
                                 dbg_keys, ws_ptr(workspace), stream)
 
 
+    def decode_dev(self, rope: bd.SkvRope, q, k_new, v_new, step_dev, max_step: int, out, workspace,
+                   sel_ids=None, dbg_keys=None, stream=None):
+        """Graph-replayable decode: the step index is read on the device from step_dev (int32 tensor)."""
+        bd.shadowkv_decode_step_dev(self.shape.dims(), rope, self.layer(), q, k_new, v_new, step_dev, max_step, out,
+                                    sel_ids, dbg_keys, ws_ptr(workspace), stream)
+
+
 class RopeTable:
     """Device copy of the model's fp32 inv_freq table + layout flags (skv_rope)."""
 

@@ -208,3 +208,45 @@ def test_full_size_sampled(name):
     sub = cfg.replace(batch=len(sample))
     check_decode(sub, f64(out[sample]), sel[sample].cpu().numpy(), f64(dbg[sample]), oout, osel, oz, okeys)
     assert torch.isfinite(out.float()).all()                      # the unsampled requests ran too
+
+
+@pytest.mark.parametrize("name", ["c1", "g8_ragged"])
+def test_decode_step_dev_and_graph_replay(name):
+    """shadowkv_decode_step_dev (step read on the device, grid sized for max_step) and one captured CUDA
+    graph replayed across steps give bit-identical outputs to shadowkv_decode_step."""
+    P = Problem(CASES[name], seed=8, steps=5)
+    ost = P.oracle_build()
+    P.load_state_from_oracle(ost)
+    c = P.cfg
+    max_step = 3
+    steps = [P.step_inputs(s) for s in range(4)]
+    ref = []
+    for s, si in enumerate(steps):
+        out = torch.empty(c.batch, c.n_q_heads, c.head_dim, dtype=torch.bfloat16, device="cuda")
+        P.st.decode(P.rope.struct, si["q"].cuda(), si["k_new"].cuda(), si["v_new"].cuda(), s, out, P.ws)
+        ref.append(out.clone())
+    step_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for s, si in enumerate(steps):                        # device step, plain launches
+        step_dev.fill_(s)
+        out = torch.empty_like(ref[0])
+        P.st.decode_dev(P.rope.struct, si["q"].cuda(), si["k_new"].cuda(), si["v_new"].cuda(), step_dev, max_step,
+                        out, P.ws)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref[s]), f"step_dev decode differs at step {s}"
+    q_b = steps[0]["q"].cuda().clone(); k_b = steps[0]["k_new"].cuda().clone(); v_b = steps[0]["v_new"].cuda().clone()
+    out_b = torch.empty_like(ref[0])
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        step_dev.fill_(0)
+        P.st.decode_dev(P.rope.struct, q_b, k_b, v_b, step_dev, max_step, out_b, P.ws, stream=side)   # warm-up
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            P.st.decode_dev(P.rope.struct, q_b, k_b, v_b, step_dev, max_step, out_b, P.ws, stream=side)
+            step_dev.add_(1)
+        step_dev.fill_(0)
+        for s, si in enumerate(steps):
+            q_b.copy_(si["q"]); k_b.copy_(si["k_new"]); v_b.copy_(si["v_new"])
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out_b, ref[s]), f"graph replay differs at step {s}"
