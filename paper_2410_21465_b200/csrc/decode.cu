@@ -250,7 +250,7 @@ __device__ __forceinline__ int block_sum(int x, int* wsum) {
 template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 2)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
-         int score_total, int score_grid, float* __restrict__ zws, int32_t* __restrict__ sel,
+         int score_total, int score_grid, int parts_per_cta, float* __restrict__ zws, int32_t* __restrict__ sel,
          int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int early_trigger,
          int force_fb) {
   TRACE_INIT;
@@ -286,7 +286,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   // ---- lse_hq from the score CTAs' per-segment partials: max-reduce, one exp per lane, sum-reduce
   //      (short dependent chains; fixed order, deterministic)
   if (warp < G) {
-    const int nseg = seg_count((int)bh, tiles_per_head, score_total, score_grid);
+    const int nseg = parts_per_cta * seg_count((int)bh, tiles_per_head, score_total, score_grid);
     if (warp == 0) trace(1, 13);
     const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * kSegMax;
     float2 v0 = lane < nseg ? ph[lane] : make_float2(-INFINITY, 0.f);
@@ -976,6 +976,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   while (grid_s > 1 && (long long)tph * grid_s / total_tiles + 2 > kSegMax) --grid_s;   // select's slots
   // a1: tcgen05 score (TMA + TMEM); CUDA-core fallback when tensor maps are unavailable
   int score_grid = score_tc_grid(D, tph, num_sms());
+  int parts_per_cta = 2;                                // k_score_tc: one softmax partial per epilogue group
   const char* nt = getenv("SKV_NO_TC");                 // test hook: force the CUDA-core score
   e = (nt && nt[0] == '1') ? cudaErrorNotSupported
                            : launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
@@ -984,6 +985,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
     cudaGetLastError();
     score_grid = grid_s;
+    parts_per_cta = 1;
     if (prof) profile_mark(prof, kScore, false, st);
     k_score<G><<<grid_s, 256, score_smem, st>>>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
                                                 v_new, Ly.K_win, Ly.V_win, step);
@@ -998,10 +1000,10 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     const bool zsm = z_fits_smem(D, G);
     const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
     if (zsm) e = launch_pdl(k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
-                            (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
+                            (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, parts_per_cta, ws.z,
                             ws.sel, ws.selrest, ws.flags, sel_ids, early_sel, force_fb);
     else e = launch_pdl(k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
-                        (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, ws.z,
+                        (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, parts_per_cta, ws.z,
                         ws.sel, ws.selrest, ws.flags, sel_ids, early_sel, force_fb);
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }

@@ -29,7 +29,7 @@ constexpr int kTcStages = 6;
 constexpr int kTcAcc = 8;                 // TMEM accumulator buffers (16 fp32 columns each)
 constexpr int kTcMaxHeads = 4;            // KV heads a CTA's contiguous tile range may touch
 constexpr int kTcMaxTiles = 64;           // tiles per CTA (bitmap size); host sizes the grid accordingly
-constexpr int kTcThreads = 224;         // 4 epilogue warps, 1 TMA producer, 2 MMA issuers
+constexpr int kTcThreads = 352;         // 2 x 4 epilogue warps, 1 TMA producer, 2 MMA issuers
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
 
@@ -115,7 +115,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], acc_full[kTcAcc], acc_empty[kTcAcc];
   __shared__ uint32_t tmem_base;
   __shared__ uint32_t obits[kTcMaxTiles * (kSTile / 32)];
-  __shared__ float2 wpart[4][16];
+  __shared__ float2 wpart[2][4][16];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = D.b * D.hk * tiles_per_head;
   const int t_begin = (int)((long long)blockIdx.x * total / gridDim.x);
@@ -236,51 +236,59 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       }
     }
   } else {
-    // ---------------- epilogue: warps 0-3, TMEM lanes 32w .. 32w+31 ----------------
-    // per-thread online softmax partials over the CTA's rows of each KV head, merged across the 4
-    // epilogue warps once per head segment: one partial per (CTA, KV head) at slot = CTA index minus
-    // the first CTA that covers the head (seg_first(); k_select recomputes the same mapping)
-    // Branch-free online update in the log2 domain, one independent chain per head (ILP): the four
-    // epilogue warps sit one per sub-partition, so dependent latency, not issue, paces them.
-    // A finite floor stands in for -inf so that fully masked rows never produce inf - inf.
+    // ---------------- epilogue: two groups of 4 warps (0-3 and 7-10) on alternate tiles ----------------
+    // Warp w reads TMEM lane quadrant w % 4.  A single warp per sub-partition was latency / issue bound
+    // (~1000 cycles per tile at G = 16); two groups halve the per-tile work of each.  Each group keeps
+    // per-thread online softmax partials over its rows of each KV head and flushes one partial per
+    // (CTA, KV head, group) at slot 2 * (CTA index - seg_first()) + group (k_select reads 2 per CTA);
+    // a group flushes an empty partial for every head of the CTA's range it saw no tile of, so the
+    // slot set stays complete and both groups pass the same named barriers.
+    // Branch-free online update in the log2 domain, one independent chain per head (ILP); a finite
+    // floor stands in for -inf so that fully masked rows never produce inf - inf.
     constexpr float kFloor = -1e30f, kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
+    const int grp = warp >= 7 ? 1 : 0, quad = warp & 3;
     float m_run[G], s_run[G];
 #pragma unroll
     for (int hq = 0; hq < G; ++hq) { m_run[hq] = kFloor; s_run[hq] = 0.f; }
     auto flush = [&](int bh) {
       const int b = bh / D.hk, h = bh - b * D.hk;
-      const int slot = (int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x);
+      const int slot = 2 * ((int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x)) + grp;
 #pragma unroll
       for (int hq = 0; hq < G; ++hq) {
         const float m2 = warp_max(m_run[hq]);
         const float sm = warp_sum(s_run[hq] * exp2f(m_run[hq] - m2));
-        if (lane == 0) wpart[warp][hq] = m2 > kFloor ? make_float2(m2 * kLn2, sm) : make_float2(-INFINITY, 0.f);
+        if (lane == 0) wpart[grp][quad][hq] = m2 > kFloor ? make_float2(m2 * kLn2, sm) : make_float2(-INFINITY, 0.f);
         m_run[hq] = kFloor; s_run[hq] = 0.f;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");     // the 4 epilogue warps
-      if (warp == 0 && lane < G) {
+      if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");   // the group's 4 warps
+      else asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (quad == 0 && lane < G) {
         float m = -INFINITY, sm = 0.f;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) lse_merge(m, sm, wpart[w][lane].x, wpart[w][lane].y);
+        for (int w = 0; w < 4; ++w) lse_merge(m, sm, wpart[grp][w][lane].x, wpart[grp][w][lane].y);
         part[((size_t)b * D.hq + (size_t)h * G + lane) * kSegMax + slot] = make_float2(m, sm);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+      else asm volatile("bar.sync 2, 128;" ::: "memory");
     };
+    const int bh_last = (t_end - 1) / tiles_per_head;
     int bh = t_begin / tiles_per_head, tile = t_begin - bh * tiles_per_head;   // advanced incrementally
-    int cur_bh = bh;
+    if (grp == 1 && ntile > 1) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
+    int cur_bh = t_begin / tiles_per_head;
     float* lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
-    const int r = 32 * warp + lane;
-    for (int i = 0; i < ntile; ++i) {
+    const int r = 32 * quad + lane;
+    for (int i = grp; i < ntile; i += 2) {
       const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
       if (bh != cur_bh) {
-        flush(cur_bh);
+        flush(cur_bh);                                    // (and empty partials for heads skipped)
+        for (int e = cur_bh + 1; e < bh; ++e) flush(e);
         cur_bh = bh;
         lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
       }
       mbar_wait(&acc_full[buf], aph);
       tc_fence_after();
       float v[16];
-      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + buf * 16, v);
+      tmem_ld16(tmem + ((uint32_t)(32 * quad) << 16) + buf * 16, v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
@@ -298,10 +306,11 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
           m_run[hq] = mn;
         }
       }
-      if (++tile == tiles_per_head) { tile = 0; ++bh; }
+      for (int st2 = 0; st2 < 2; ++st2) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
     }
     if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 13);     // epilogue loop done
     flush(cur_bh);
+    for (int e = cur_bh + 1; e <= bh_last; ++e) flush(e);          // heads this group saw no tile of
     if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 14);     // partials flushed
   }
   __syncthreads();
@@ -341,7 +350,7 @@ int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm) {
                           (total + grid - 1) / grid > kTcMaxTiles))
     grid = grid * 2 < total ? grid * 2 : total;
   // at most kSegMax score CTAs may cover one KV head (k_select's partial slots)
-  while (grid > 1 && (long long)tiles_per_head * grid / total + 2 > kSegMax) --grid;
+  while (grid > 1 && 2 * ((long long)tiles_per_head * grid / total + 2) > kSegMax) --grid;   // 2 per CTA
   return grid;
 }
 
