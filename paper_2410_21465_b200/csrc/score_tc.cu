@@ -33,10 +33,17 @@ constexpr int kTcThreads = 352;         // 2 x 4 epilogue warps, 1 TMA producer,
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// Landmarks are streamed once per decode step and never re-read within it: load them with an L2
+// evict-first policy so that they do not push the freshly written logits (re-read by k_select) and
+// the small per-step state out of L2 (c3/c5 stream 0.2-2 GB of landmarks per layer through 126 MB).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t p; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p;
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 
@@ -123,6 +130,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   const int ntile = t_end - t_begin;
   const int bh0 = t_begin / tiles_per_head;
   uint64_t* const trace_buf = g_trace_tc ? g_trace_tc + (size_t)D.trace_slot * kTraceSlot : nullptr;
+  const uint64_t pol = l2_evict_first_policy();
   trace_tc(trace_buf, 0);
   if (early_trigger) pdl_trigger();
   // the producer thread initialises the barriers and puts the first kTcStages tiles in flight
@@ -144,8 +152,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
       const int row0 = bh * D.n_c + tile * kSTile;
       mbar_expect_tx(&full[i], kTileBytes);
-      tma_load_2d(sA + i * kTileBytes, &tmap, 0, row0, &full[i]);
-      tma_load_2d(sA + i * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[i]);
+      tma_load_2d(sA + i * kTileBytes, &tmap, 0, row0, &full[i], pol);
+      tma_load_2d(sA + i * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[i], pol);
     }
   }
   if (ntile <= 0) { pdl_wait(); return; }
@@ -208,8 +216,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
         const int row0 = bh * D.n_c + tile * kSTile;
         mbar_expect_tx(&full[s], kTileBytes);
-        tma_load_2d(sA + s * kTileBytes, &tmap, 0, row0, &full[s]);
-        tma_load_2d(sA + s * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[s]);
+        tma_load_2d(sA + s * kTileBytes, &tmap, 0, row0, &full[s], pol);
+        tma_load_2d(sA + s * kTileBytes + kTileBytes / 2, &tmap, 64, row0, &full[s], pol);
       }
     }
   } else if (warp == 5 || warp == 6) {
