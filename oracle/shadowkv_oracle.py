@@ -26,7 +26,7 @@ __all__ = [
     "bf16_round", "identity_store", "partition", "rope", "chunk_means", "chunk_min_cos",
     "smallest_o", "build", "BuildState", "landmark_scores", "normalise_group_max",
     "arg_topk", "rebuild_keys", "decode_step", "dense_attention", "softmax_attention",
-    "equivalent_bandwidth", "jacobi_svd",
+    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits",
 ]
 
 
@@ -280,6 +280,55 @@ def dense_attention(q, keys, values):
         for t in range(keys.shape[1]):
             out[hq] += p[t] * values[h, t]
     return out
+
+
+# ----------------------------------------------------------------------------
+# value-chunk cache with temporal locality
+# ----------------------------------------------------------------------------
+class ValueChunkCache:
+    """GPU-resident cache of selected value chunks for one (request, layer, KV head).
+
+    P:105 "considering the temporal locality of the KV cache, a cache policy can be leveraged";
+    P:156 "we conduct an index scan to detect the missed chunks and only rebuild the necessary KV
+    pairs".  The paper names no policy (it cites PQCache); SPEC S:139-146, S:158 fix it as
+    least-recently-SELECTED replacement at chunk granularity with capacity defaulting to the budget
+    k (DESIGN reading R26).  ``fetch`` follows S:139-143 literally: the hit flags are true exactly for
+    the ids resident before the call; every requested id becomes most recent; the misses are
+    inserted in ascending id order, evicting least-recently-selected chunks while over capacity.
+    Values themselves are bit copies of V rows ("round-trip fidelity"), so only the hit
+    pattern is modelled here.
+    """
+
+    def __init__(self, capacity: int):
+        self.capacity = int(capacity)
+        self.last_use = {}            # chunk id -> call index of its last selection
+        self.calls = 0
+        self.hits = 0
+        self.requested = 0
+
+    def fetch(self, ids):
+        ids = [int(i) for i in ids]
+        assert len(set(ids)) == len(ids), "duplicate chunk id in one fetch"
+        hit = np.array([i in self.last_use for i in ids], dtype=bool)
+        t = self.calls
+        self.calls += 1
+        for i in sorted(ids):                        # every requested chunk is now most recent
+            self.last_use[i] = t
+        while len(self.last_use) > self.capacity:    # evict least recently selected (ties: lower id)
+            victim = min(self.last_use, key=lambda j: (self.last_use[j], j))
+            del self.last_use[victim]
+        self.hits += int(hit.sum())
+        self.requested += len(ids)
+        return hit
+
+    def hit_rate(self) -> float:
+        return self.hits / self.requested if self.requested else 0.0
+
+
+def replay_hits(trace, capacity: int):
+    """Per-step hit counts of a selection trace [steps][k] through one ValueChunkCache."""
+    cache = ValueChunkCache(capacity)
+    return np.array([int(cache.fetch(ids).sum()) for ids in trace], dtype=np.int64)
 
 
 def equivalent_bandwidth(S, C, K, O, alpha, B_gpu, B_pcie):

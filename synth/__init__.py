@@ -16,6 +16,9 @@ Recipe:
   * B [b][h_kv][r][d]: N(0, 1/r)  -> key entries ~ unit variance.
   * V [b][h_kv][s][d]: N(0, 1).
   * q [b][h_q][d]: N(0, tau^2), tau = 2.  k_new, v_new [b][h_kv][d]: N(0, 1).
+  * Temporally correlated queries (value-cache runs, DESIGN R27): q_t = rho q_{t-1} +
+    sqrt(1 - rho^2) tau eps_t per (request, q head), stationary N(0, tau^2) marginals; rho sets
+    how much consecutive selections overlap (the paper's Fig 3c hit rate).
   * Everything is rounded to bf16 once.
   * RoPE tables: Llama-3.1 (base 5e5, llama3 scaling, halves layout, full d)
     for the Llama shapes; GLM-4 (rotary_dim 64, interleaved, base 1e4*1e4).
@@ -28,7 +31,7 @@ import math
 import numpy as np
 import torch
 
-__all__ = ["Config", "CONFIGS", "rope_table", "gen_layer", "gen_step", "stream_seed"]
+__all__ = ["Config", "CONFIGS", "rope_table", "gen_layer", "gen_step", "gen_q_drift", "stream_seed"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -163,3 +166,20 @@ def gen_step(cfg: Config, seed: int, layer: int = 0, step: int = 0, device="cpu"
     kn = torch.randn(b, cfg.n_kv_heads, cfg.head_dim, generator=g, device=device).to(torch.bfloat16)
     vn = torch.randn(b, cfg.n_kv_heads, cfg.head_dim, generator=g, device=device).to(torch.bfloat16)
     return {"q": q, "k_new": kn, "v_new": vn}
+
+
+def gen_q_drift(cfg: Config, seed: int, layer: int, steps: int, rho: float, device="cpu",
+                batch: int | None = None, tau: float = 2.0) -> torch.Tensor:
+    """Queries of ``steps`` consecutive decode steps as a stationary AR(1) process over the step
+    index (fp32, rounded to bf16 once): q_0 ~ N(0, tau^2); q_t = rho q_{t-1} + sqrt(1-rho^2) tau eps_t.
+    Returns bf16 [steps][b][h_q][d].  rho = 0 gives independent queries (like gen_step's)."""
+    b = cfg.batch if batch is None else batch
+    g = _gen(stream_seed(seed, layer, 3), device)
+    shape = (b, cfg.n_q_heads, cfg.head_dim)
+    out = torch.empty((steps,) + shape, dtype=torch.bfloat16, device=device)
+    cur = tau * torch.randn(shape, generator=g, device=device)
+    for t in range(steps):
+        if t:
+            cur = rho * cur + math.sqrt(1.0 - rho * rho) * tau * torch.randn(shape, generator=g, device=device)
+        out[t] = cur.to(torch.bfloat16)
+    return out
