@@ -51,6 +51,10 @@ def parse():
                          "counter) instead of per-call stream launches")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: every rank runs the config's batch; strong: the batch is split over ranks")
+    ap.add_argument("--vc-rho", default="0.95",
+                    help="value-cache leg (P:156, DESIGN R26/R27): comma list of query-drift correlations rho; "
+                         "each runs the same step with a GPU value cache per layer and drifting queries and "
+                         "reports the measured hit rate alpha ('' = skip)")
     ap.add_argument("--layer-states", type=int, default=0,
                     help="distinct layer states cycled per step (default: the model's layer count)")
     return ap.parse_args()
@@ -264,6 +268,75 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------------------------------------
+def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_bytes, host_peak, n_total, dev):
+    """NEXT-1: the same 32-layer step with a GPU value-chunk cache per layer (skv_layer.vc_*,
+    capacity k chunks per request and KV head, DESIGN R26) and temporally correlated queries (AR(1) drift
+    over decode steps, synth.gen_q_drift, R27).  Hit rate alpha is read from the kernels' own counters.
+    Timed like the main pass: one CUDA graph per step, W warm-up replays (which also fill the cache),
+    K timed replays with CUDA events."""
+    import copy
+    from paper_2410_21465_b200 import binding as bd
+    Lm, b = cfg.n_layers, cfg.batch
+    n_states = len(states)
+    steps, warm = args.steps, max(args.warmup, 3)
+    try:
+        layers = []
+        for l in range(Lm):                    # each layer its own cache, even where layer states are shared
+            st = copy.copy(states[l % n_states])
+            st.vc_values = torch.empty(b, cfg.n_kv_heads, 2, cfg.budget * cfg.chunk, cfg.head_dim,
+                                       dtype=torch.bfloat16, device=dev)
+            st.vc_dir = torch.zeros(b, cfg.n_kv_heads, st.shape.n_c, dtype=torch.int64, device=dev)
+            st.vc_stats = torch.zeros(b, cfg.n_kv_heads, 4, dtype=torch.int64, device=dev)
+            layers.append(st)
+        qd = torch.stack([synth.gen_q_drift(cfg, seed + 104729, l, warm + steps, rho, device=dev)
+                          for l in range(Lm)], dim=1)               # [step][layer][b][hq][d]
+    except torch.OutOfMemoryError:
+        return {"skipped": "out of HBM for per-layer caches", "q_drift_rho": rho}
+    kv = [synth.gen_step(cfg, seed, l, 0, device=dev) for l in range(Lm)]
+    k_g = torch.stack([x["k_new"] for x in kv]); v_g = torch.stack([x["v_new"] for x in kv])
+    q_g = torch.empty_like(qd[0])
+    step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+    cap = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        for l in range(Lm):
+            layers[l].decode_dev(rope.struct, q_g[l], k_g[l], v_g[l], step_dev, n_total, out[l], ws, stream=cap)
+        step_dev.add_(1)
+    for st in layers:
+        st.vc_dir.zero_(); st.vc_stats.zero_()
+    step_dev.fill_(0)
+    torch.cuda.synchronize()
+    for i in range(warm):
+        q_g.copy_(qd[i], non_blocking=True)
+        g.replay()
+    torch.cuda.synchronize()
+    h0 = sum(int(st.vc_stats[..., 3].sum()) for st in layers)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(warm, warm + steps):
+        q_g.copy_(qd[i], non_blocking=True)
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    hits = sum(int(st.vc_stats[..., 3].sum()) for st in layers) - h0
+    lookups = steps * Lm * b * cfg.n_kv_heads * cfg.budget
+    alpha = hits / lookups
+    miss_bytes = (1.0 - alpha) * host_bytes                          # host-link bytes per layer call
+    t_roof = Lm * miss_bytes / (host_peak * 1e9)
+    del g, layers, qd
+    torch.cuda.empty_cache()
+    from paper_2410_21465_b200 import shard
+    value = shard.job_tokens_per_s(b, ms / 1e3, device=dev)             # all ranks: sum tokens / max time
+    return {"q_drift_rho": rho, "alpha": alpha, "value": value, "unit": UNIT, "ms_per_step": ms,
+            "steps": steps, "warmup": warm, "host_bytes_per_layer": miss_bytes,
+            "step_frac_of_host_roofline": t_roof / (ms * 1e-3),
+            "note": "P:156 cache-aware decode: chunks selected in the previous step come from HBM (capacity k, "
+                    "least-recently-selected == previous selection); alpha measured by the kernels' hit counters; "
+                    "queries drift as AR(1) over steps (synthetic: the paper's ~60% is Fig 3c on real traces)"}
+
+
+# ------------------------------------------------------------------------------------------------
 def run_ours(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -448,6 +521,11 @@ def run_ours(args, cfg):
                 "peak_note": "pinned H2D copy-engine bandwidth measured live in this run (1 GiB, best of 6); "
                              "zero-copy SM loads saturate ~51 GB/s (profiles/r01_probe_hostlink.txt)"}
 
+    value_cache = None
+    if args.vc_rho:
+        value_cache = [value_cache_leg(args, cfg, float(r), states, rope, ws, out, stream, seed, host_bytes, host_peak,
+                                       n_total, dev) for r in args.vc_rho.split(",") if r.strip()]
+
     breakdown = None
     if args.breakdown:
         bd.shadowkv_profile_begin(Lm * 5 * 20 + 8, 0x1F)
@@ -473,6 +551,8 @@ def run_ours(args, cfg):
             "clocks": clk.summary(),
             "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
             "setup_s": setup_s}
+    if value_cache:
+        line["value_cache"] = value_cache[0] if len(value_cache) == 1 else value_cache
     if breakdown:
         line["kernel_breakdown_us"] = breakdown
     if world == 1 and not args.no_cpu_baseline:

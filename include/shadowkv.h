@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SHADOWKV_ABI_VERSION 1
+#define SHADOWKV_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SKV_API __attribute__((visibility("default")))
@@ -92,6 +92,22 @@ typedef struct {
   uint16_t *V_win;          /* device bf16 [b][h_kv][window_cap][d]                             */
   /* offloaded values V^CPU: all s positions kept; outlier/window rows are never read */
   const uint16_t *V_host;   /* host-mapped bf16 [b][h_kv][s][d], read zero-copy over PCIe        */
+  /* Optional GPU-resident value-chunk cache ("considering the temporal locality of the KV
+   * cache, a cache policy can be leveraged"; "we conduct an index scan to detect the missed
+   * chunks"; policy per SPEC S:139-146, DESIGN R26): least-recently-selected replacement,
+   * capacity = the budget k chunks per (request, KV head).  With capacity k the cache after a step
+   * holds exactly that step's selection, so it is kept as two slot buffers that alternate by step
+   * (read the previous step's, write this step's).  A selected chunk whose directory entry carries
+   * the previous generation's tag is a HIT: its values are copied from HBM instead of the host link.
+   * Every selected chunk's values are written to this step's buffer.  Values are bit copies either
+   * way, so outputs do not depend on the cache state.  All three NULL = no cache; all three or none.
+   * build_cache zero-fills vc_dir and vc_stats (a new prefill starts cold); a caller may also reset
+   * the cache by zero-filling both.  Not shared between layers. */
+  uint16_t *vc_values;      /* device bf16 [b][h_kv][2][k*c][d] (two slot buffers per KV head)     */
+  uint64_t *vc_dir;         /* device [b][h_kv][n_c]: (tag << 32) | slot; tag = generation + 1 of
+                               the step that last wrote the chunk; zero = never cached          */
+  uint64_t *vc_stats;       /* device [b][h_kv][4]: {generation (decode steps run), scratch,
+                               hits in the last step, hits in total}; read them after a sync    */
 } skv_layer;
 
 /* Bytes of scratch `workspace` (device, 256-byte aligned) that build_cache and decode_step need
@@ -109,6 +125,7 @@ SKV_API size_t shadowkv_workspace_bytes(const skv_dims *dims);
  *   outlier_ids <- the o chunks with smallest m (ties -> lower j, R12), ascending
  *   K_out, V_out <- keys / values of those chunks; values read zero-copy from V_host
  *   K_win, V_win slots [0, w_eff) <- the context tail (R8)
+ * With a value cache (vc_*), zero-fills vc_dir and vc_stats (cold cache for the new context).
  * Requires V_host page-locked and mapped (checked once here; SKV_ESTATE otherwise). */
 SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
                                 const uint16_t *K_rope, void *workspace, void *stream);
@@ -119,7 +136,9 @@ SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *ro
  *   a2  z_{h,j} = max_{hq in group h} (l_{hq,j} - logsumexp_j l_{hq,.})  (= log S2, R4, R5)
  *   a3  I_h = ArgTopK(z_h, k), ties -> lower chunk id, ascending (R12)
  *   a4  K~ = RoPE_t(A[t] . B_h) for the k*c tokens of I_h at their absolute positions
- *   a5  V~ = V_host rows of those tokens, gathered zero-copy over the host link
+ *   a5  V~ = V_host rows of those tokens, gathered zero-copy over the host link; with a
+ *       value cache, chunks selected in the previous step are copied from vc_values instead, and
+ *       every selected chunk is written to this step's slot buffer (R26)
  *   a6  out_hq = softmax attention of q_hq over outlier tokens + K~/V~ + window slots
  *       [0, w_eff+step] (R17)
  * q      device bf16 [b][h_q][d], post-RoPE at position s+step (R16)

@@ -544,7 +544,8 @@ __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
 template <int G>
 __global__ void __launch_bounds__(kHeadDim)
 k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_part, int n_split,
-        int32_t* __restrict__ sel, int* __restrict__ flags, uint16_t* __restrict__ out, int late_trigger) {
+        int32_t* __restrict__ sel, int* __restrict__ flags, uint16_t* __restrict__ out, int late_trigger,
+        unsigned long long* __restrict__ vc_stats) {
   TRACE_INIT;
   extern __shared__ __align__(16) float2 mls[];          // [n_split]
   const int row = blockIdx.x, d = threadIdx.x;            // row = b * hq + hq
@@ -604,6 +605,11 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
     int32_t* slots = sel + (size_t)bh * D.k;
     for (int i = d; i < D.k; i += kHeadDim) slots[i] = 0;
     if (d < 4) flags[(size_t)bh * 4 + d] = 0;
+    if (vc_stats && d == 0) {                             // value cache: close the generation (R26)
+      unsigned long long* st = vc_stats + (size_t)bh * 4;
+      const unsigned long long hits = __ldcg(st + 1);
+      st[1] = 0; st[2] = hits; st[3] += hits; st[0] += 1;
+    }
   }
 }
 
@@ -649,6 +655,8 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
   __syncthreads();
   int ntok;
+  int vc_id = -1;                              // value cache: this thread's chunk and the call's generation
+  unsigned long long vc_gen = 0;
   const int tx = tid & 15, ty = tid >> 4;      // key-tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
   float acc[4][8];
   if (kind == 0) {
@@ -664,16 +672,30 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       int v;
       while ((v = ld_relaxed_gpu(sp)) == 0) __nanosleep(32);
       const int id = v - 1;
+      vc_id = id;
 #pragma unroll
       for (int e = 0; e < kChunk; ++e) tok[tid * kChunk + e] = id * kChunk + e;
       const uint32_t rb = kChunk * D.r * 2;
       // a4 operands (HBM): 8 contiguous factor rows (2.5 KB at r = 160)
       mbar_expect_tx(&barAB, rb);
       bulk_g2s(As + tid * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)id * kChunk) * D.r, rb, &barAB);
-      // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy)
+      // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy) -- or,
+      // with the value cache, from HBM when the chunk was selected in the previous step ("index
+      // scan to detect the missed chunks": one directory probe per selected chunk, R26)
+      const uint16_t* vsrc = Ly.V_host + ((size_t)bh * D.s + (size_t)id * kChunk) * kHeadDim;
+      if (Ly.vc_dir) {
+        (void)ld_acquire_gpu(sp);            // order the probes after the publication (which follows
+                                             // the previous call's generation bump)
+        vc_gen = ld_relaxed_gpu_u64(Ly.vc_stats + (size_t)bh * 4);
+        const unsigned long long e = ld_relaxed_gpu_u64(Ly.vc_dir + (size_t)bh * D.n_c + id);
+        const unsigned tag = (unsigned)vc_gen;
+        if (tag != 0u && (unsigned)(e >> 32) == tag) {
+          vsrc = Ly.vc_values + (((size_t)bh * 2 + ((vc_gen - 1) & 1)) * D.k + (unsigned)e) * (kChunk * kHeadDim);
+          atomicAdd(Ly.vc_stats + (size_t)bh * 4 + 1, 1ull);
+        }
+      }
       mbar_expect_tx(&barV, kChunk * kHeadDim * 2);
-      bulk_g2s(Vs + tid * kChunk * kHeadDim, Ly.V_host + ((size_t)bh * D.s + (size_t)id * kChunk) * kHeadDim,
-               kChunk * kHeadDim * 2, &barV);
+      bulk_g2s(Vs + tid * kChunk * kHeadDim, vsrc, kChunk * kHeadDim * 2, &barV);
     } else if (tid < kUnitTok && tid >= nch * kChunk) {
       tok[tid] = 0;                                      // padded rows (masked below)
     }
@@ -837,6 +859,13 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   trace(2, 4);
   mbar_wait(&barV, 0);                                   // values (from PCIe for selected units)
   trace(2, 5);
+  if (vc_id >= 0 && Ly.vc_dir) {                         // this step's selection becomes the cache (R26)
+    const int slot = ui * 8 + tid;                       // deterministic position in the selection
+    fence_proxy_async();
+    bulk_s2g(Ly.vc_values + (((size_t)bh * 2 + (vc_gen & 1)) * D.k + slot) * (kChunk * kHeadDim),
+             Vs + tid * kChunk * kHeadDim, kChunk * kHeadDim * 2);
+    Ly.vc_dir[(size_t)bh * D.n_c + vc_id] = ((vc_gen + 1) << 32) | (unsigned)slot;
+  }
   __syncthreads();
   // ---- PV: thread = (dim pair, head group of 4): bf16x2 value loads, float4 probability loads
   {
@@ -861,6 +890,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       if (dp == 0) ml_part[row] = ml[hq];
     }
   }
+  if (vc_id >= 0 && Ly.vc_dir) bulk_wait_read();         // the cache write-back has read its smem
   trace(2, 8);
 }
 
@@ -1028,7 +1058,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (prof) profile_mark(prof, kCombine, false, st);
   if ((e = launch_pdl(k_merge<G>, dim3(D.b * D.hq), dim3(kHeadDim), (size_t)n_split * (sizeof(float2) + sizeof(float)), st, D,
                       (const float*)ws.o_part, (const float2*)ws.ml_part, n_split, ws.sel, ws.flags, out,
-                      merge_late))) return e;
+                      merge_late, Ly.vc_stats))) return e;
   if (prof) profile_mark(prof, kCombine, true, st);
   *launches += 4;
   return cudaGetLastError();
@@ -1121,6 +1151,11 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
     L.K_win = Ly.K_win + (size_t)r0 * hk * D.wcap * d;
     L.V_win = Ly.V_win + (size_t)r0 * hk * D.wcap * d;
     L.V_host = Ly.V_host + (size_t)r0 * hk * s * d;
+    if (Ly.vc_dir) {
+      L.vc_values = Ly.vc_values + (size_t)r0 * hk * 2 * D.k * kChunk * d;
+      L.vc_dir = Ly.vc_dir + (size_t)r0 * hk * D.n_c;
+      L.vc_stats = Ly.vc_stats + (size_t)r0 * hk * 4;
+    }
     DecodeWs ws;
     decode_ws_bytes(Ds, &ws, ws_base + offs[i]);
     cudaStream_t si = i == 0 ? st : side[i - 1];

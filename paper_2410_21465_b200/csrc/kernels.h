@@ -27,6 +27,10 @@ struct Layer {
   int32_t* outlier_ids;
   uint16_t *K_out, *V_out, *K_win, *V_win;
   const uint16_t* V_host;
+  // optional value-chunk cache (R26); all null = off
+  uint16_t* vc_values;                // [b][hk][2][k*c][d]
+  unsigned long long* vc_dir;         // [b][hk][n_c]  (tag << 32) | slot
+  unsigned long long* vc_stats;       // [b][hk][4]    {generation, step hits (scratch), last hits, total hits}
 };
 
 // workspace carving (256-B aligned regions)

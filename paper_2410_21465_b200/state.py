@@ -61,7 +61,8 @@ def ws_ptr(ws: torch.Tensor) -> int:
 class LayerState:
     """One layer's tensors for the whole per-GPU batch."""
 
-    def __init__(self, shape: Shape, device="cuda", V_host: torch.Tensor | None = None):
+    def __init__(self, shape: Shape, device="cuda", V_host: torch.Tensor | None = None,
+                 value_cache: bool = False):
         self.shape = S = shape
         b, hk, d = S.batch, S.n_kv_heads, S.head_dim
         bf = torch.bfloat16
@@ -78,10 +79,21 @@ class LayerState:
             V_host = torch.empty(b, hk, S.ctx_len, d, dtype=bf, pin_memory=True)
         assert V_host.is_pinned() and V_host.shape == (b, hk, S.ctx_len, d)
         self.V_host = V_host
+        # optional GPU-resident value-chunk cache (skv_layer.vc_*, DESIGN R26): two slot buffers of
+        # k chunks per (request, KV head), the chunk directory and the hit counters
+        self.vc_values = self.vc_dir = self.vc_stats = None
+        if value_cache:
+            self.vc_values = torch.empty(b, hk, 2, S.budget * S.chunk, d, dtype=bf, device=device)
+            self.vc_dir = torch.zeros(b, hk, S.n_c, dtype=torch.int64, device=device)
+            self.vc_stats = torch.zeros(b, hk, 4, dtype=torch.int64, device=device)
 
     def layer(self) -> bd.SkvLayer:
         return bd.layer_struct(self.A, self.B, self.landmarks, self.outlier_ids, self.K_out, self.V_out,
-                               self.K_win, self.V_win, self.V_host)
+                               self.K_win, self.V_win, self.V_host, self.vc_values, self.vc_dir, self.vc_stats)
+
+    def cache_stats(self):
+        """-> int64 [b][h_kv][4] {generation, -, hits in the last step, hits in total} (synchronises)."""
+        return None if self.vc_stats is None else self.vc_stats.cpu()
 
     def build(self, rope: bd.SkvRope, workspace: torch.Tensor, K_rope: torch.Tensor | None = None, stream=None):
         bd.shadowkv_build_cache(self.shape.dims(), rope, self.layer(), K_rope, ws_ptr(workspace), stream)

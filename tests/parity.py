@@ -55,13 +55,14 @@ def outliers_valid(gpu_ids: np.ndarray, m: np.ndarray, o: int, tol: float = M_TI
 class Problem:
     """Seeded synthetic inputs for one layer (synth), the GPU state and the oracle state."""
 
-    def __init__(self, cfg: synth.Config, seed: int, steps: int = 4, K_rope: bool = False, device="cuda"):
+    def __init__(self, cfg: synth.Config, seed: int, steps: int = 4, K_rope: bool = False, device="cuda",
+                 value_cache: bool = False):
         from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
         self.cfg, self.seed, self.steps = cfg, seed, steps
         self.inputs = synth.gen_layer(cfg, seed)
         self.inv, self.rot, self.il = synth.rope_table(cfg)
         self.shape = Shape.from_config(cfg, steps=steps)
-        self.st = LayerState(self.shape, device=device)
+        self.st = LayerState(self.shape, device=device, value_cache=value_cache)
         self.st.A.copy_(self.inputs["A"]); self.st.B.copy_(self.inputs["B"])
         self.st.V_host.copy_(self.inputs["V"])
         self.rope = RopeTable(self.inv, self.rot, self.il, device=device)
@@ -97,14 +98,15 @@ class Problem:
     def step_inputs(self, step):
         return synth.gen_step(self.cfg, self.seed, 0, step)
 
-    def gpu_decode(self, step, si):
+    def gpu_decode(self, step, si, st=None):
         c, b = self.cfg, self.cfg.batch
         dev = "cuda"
+        st = self.st if st is None else st
         out = torch.empty(b, c.n_q_heads, c.head_dim, dtype=torch.bfloat16, device=dev)
         sel = torch.empty(b, c.n_kv_heads, c.budget, dtype=torch.int32, device=dev)
         dbg = torch.empty(b, c.n_kv_heads, c.budget * c.chunk, c.head_dim, dtype=torch.bfloat16, device=dev)
-        self.st.decode(self.rope.struct, si["q"].to(dev), si["k_new"].to(dev), si["v_new"].to(dev), step, out,
-                       self.ws, sel_ids=sel, dbg_keys=dbg)
+        st.decode(self.rope.struct, si["q"].to(dev), si["k_new"].to(dev), si["v_new"].to(dev), step, out,
+                  self.ws, sel_ids=sel, dbg_keys=dbg)
         torch.cuda.synchronize()
         return f64(out), sel.cpu().numpy(), f64(dbg)
 

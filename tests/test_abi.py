@@ -27,7 +27,7 @@ def test_header_declares_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert bd.shadowkv_abi_version() == 1
+    assert bd.shadowkv_abi_version() == 2
 
 
 def _dims(**kw):
@@ -62,7 +62,7 @@ def test_invalid_dims_rejected(lib, kw, status, needle):
     assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(**kw))) == 0
     assert needle in lib.shadowkv_last_error().decode()
     rope = bd.SkvRope(128, 0, 16)
-    layer = bd.SkvLayer(*([16] * 9))
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 3))
     st = lib.shadowkv_decode_step(ctypes.byref(_dims(**kw)), ctypes.byref(rope), ctypes.byref(layer),
                                   16, 16, 16, 0, 16, None, None, 256, None)
     assert st == status
@@ -71,7 +71,7 @@ def test_invalid_dims_rejected(lib, kw, status, needle):
 def test_decode_argument_errors_before_any_cuda_call(lib):
     d = _dims()
     rope = bd.SkvRope(128, 0, 16)
-    layer = bd.SkvLayer(*([16] * 9))
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 3))
     call = lambda **kw: lib.shadowkv_decode_step(
         ctypes.byref(d), ctypes.byref(kw.get("rope", rope)), ctypes.byref(kw.get("layer", layer)),
         kw.get("q", 16), 16, 16, kw.get("step", 0), kw.get("out", 16), None, None, kw.get("ws", 256), None)
@@ -89,6 +89,28 @@ def test_decode_argument_errors_before_any_cuda_call(lib):
     st = lib.shadowkv_build_cache(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(bad), None, 256, None)
     assert st == bd.SKV_EINVAL
     assert lib.shadowkv_decode_step(None, None, None, 0, 0, 0, 0, 0, None, None, 0, None) == bd.SKV_EINVAL
+    partial = bd.SkvLayer(*([16] * 9 + [16, None, 16]))     # value cache: all three pointers or none
+    assert call(layer=partial) == bd.SKV_EINVAL and "vc_" in lib.shadowkv_last_error().decode()
+    misal = bd.SkvLayer(*([16] * 9 + [16, 24, 16]))
+    assert call(layer=misal) == bd.SKV_EINVAL and "aligned" in lib.shadowkv_last_error().decode()
+
+
+def test_ctypes_layer_struct_matches_header(tmp_path):
+    """The binding's skv_layer / skv_dims / skv_rope mirror the header byte for byte (C compiler's view)."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "shadowkv.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(skv_layer), offsetof(skv_layer, vc_values),'
+                   ' offsetof(skv_layer, vc_stats), sizeof(skv_dims), sizeof(skv_rope)); return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run([cc, "-I", os.path.dirname(HDR), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == [ctypes.sizeof(bd.SkvLayer), bd.SkvLayer.vc_values.offset, bd.SkvLayer.vc_stats.offset,
+                   ctypes.sizeof(bd.SkvDims), ctypes.sizeof(bd.SkvRope)]
 
 
 def test_python_binding_raises_on_error(lib):
