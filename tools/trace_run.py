@@ -18,6 +18,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--raw-epi", action="store_true", help="score events 8-11 hold clock64 deltas")
 ap.add_argument("--slots", type=int, default=1, help="trace this many consecutive layers (steady state)")
+ap.add_argument("--vc-rho", type=float, default=None, help="value cache on, queries drifting with this rho")
 args = ap.parse_args()
 os.environ["SKV_TRACE_SLOTS"] = str(args.slots)
 cfg = synth.CONFIGS[args.config]
@@ -28,7 +29,7 @@ ws = alloc_workspace(shape)
 states = []
 for l in range(args.layers):
     inp = synth.gen_layer(cfg, 99, layer=l, device="cuda")
-    st = LayerState(shape)
+    st = LayerState(shape, value_cache=args.vc_rho is not None)
     st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
     st.build(rope.struct, ws)
     states.append(st)
@@ -37,6 +38,11 @@ SLOT = 4 * 4096 * 16
 tr = torch.zeros(args.slots * SLOT, dtype=torch.int64, device="cuda")
 first = args.layers - args.slots
 sis = [[synth.gen_step(cfg, 99, l, step, device="cuda") for l in range(args.layers)] for step in range(6)]
+if args.vc_rho is not None:
+    for l in range(args.layers):
+        qd = synth.gen_q_drift(cfg, 99, l, 6, args.vc_rho, device="cuda")
+        for step in range(6):
+            sis[step][l]["q"] = qd[step]
 for step in range(6):
     for l, st in enumerate(states):
         si = sis[step][l]
@@ -49,6 +55,9 @@ for step in range(6):
         torch.cuda.synchronize()
         bd.shadowkv_trace_buffer(None)
 T = tr.view(args.slots, 4, 4096, 16).cpu().numpy().astype(np.float64)
+if args.vc_rho is not None:
+    st_ = states[-1].cache_stats()
+    print(f"value cache: last-step hit rate {st_[..., 2].sum().item() / (cfg.batch * cfg.n_kv_heads * cfg.budget):.3f}")
 g0 = T[0, 0][T[0, 0][:, 0] > 0][:, 0].min()
 if args.slots > 1:
     print("== per-layer milestones (us from the first traced layer's score start)")
