@@ -26,7 +26,7 @@ __all__ = [
     "bf16_round", "identity_store", "partition", "rope", "chunk_means", "chunk_min_cos",
     "smallest_o", "build", "BuildState", "landmark_scores", "normalise_group_max",
     "arg_topk", "rebuild_keys", "decode_step", "dense_attention", "softmax_attention",
-    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits",
+    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits", "factorize",
 ]
 
 
@@ -334,6 +334,31 @@ def replay_hits(trace, capacity: int):
 def equivalent_bandwidth(S, C, K, O, alpha, B_gpu, B_pcie):
     """Sec 4.2: B_eq = 2 S B_GPU / (S/C + 2(K+O)C + (1-alpha) K C B_GPU / B_PCIe)."""
     return 2.0 * S * B_gpu / (S / C + 2.0 * (K + O) * C + (1.0 - alpha) * K * C * B_gpu / B_pcie)
+
+
+def factorize(K_pre, r: int, svd=None):
+    """Alg 1 "A in R^{b x s x r}, B in R^{b x h_kv x r x d} <- SVD(K)", per request.
+
+    K_pre [b][h_kv][s][d] pre-RoPE keys.  Per request the keys of all KV heads are concatenated per
+    token, X[t, h*d + j] = K[h][t][j] (R14), X = U Sigma V^T, and the rank-r truncation is
+    split as A = U_r Sigma_r (shared across heads) and B_h = (V_r^T)[:, h*d:(h+1)*d].
+    ``svd`` defaults to LAPACK (numpy) as the step; the pins also run it with ``jacobi_svd``.
+    Returns (A [b][s][r], B [b][h_kv][r][d], sigma [b][min(s, h_kv*d)] descending).
+    """
+    K = np.asarray(K_pre, dtype=np.float64)
+    nb, hk, s, d = K.shape
+    A = np.zeros((nb, s, r)); B = np.zeros((nb, hk, r, d))
+    sig_all = np.zeros((nb, min(s, hk * d)))
+    for bi in range(nb):
+        X = K[bi].transpose(1, 0, 2).reshape(s, hk * d)
+        if svd is None:
+            U, sig, Vt = np.linalg.svd(X, full_matrices=False)
+        else:
+            U, sig, Vt = svd(X)
+        A[bi] = U[:, :r] * sig[:r]
+        B[bi] = Vt[:r].reshape(r, hk, d).transpose(1, 0, 2)
+        sig_all[bi] = sig[:min(s, hk * d)]
+    return A, B, sig_all
 
 
 def jacobi_svd(X, sweeps: int = 60, tol: float = 1e-15):
