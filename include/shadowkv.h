@@ -167,6 +167,27 @@ SKV_API skv_status shadowkv_decode_step_dev(const skv_dims *dims, const skv_rope
                                     const int32_t *step_dev, int32_t max_step, uint16_t *out, int32_t *sel_ids,
                                     uint16_t *dbg_keys, void *workspace, void *stream);
 
+/* Bytes of scratch `workspace` (device, 256-byte aligned) shadowkv_factorize needs for these dims
+ * (independent of batch and ctx_len: requests are factorised one after another).  0 on invalid dims. */
+SKV_API size_t shadowkv_factorize_workspace_bytes(const skv_dims *dims);
+
+/* Algorithm 1's "A, B <- SVD(K)" on the GPU, for every request, on `stream`: the rank-r
+ * truncated SVD of the pre-RoPE keys with all KV heads concatenated per token (X[t][h*d + j] =
+ * K_pre[b][h][t][j], R14), X = U S V^T, split as A = U_r S_r (shared by the heads) and
+ * B_h = (V_r^T)[:, h*d:(h+1)*d] -- exactly the factors shadowkv_build_cache / decode_step take.
+ * Computed through the D x D Gram matrix (D = h_kv*d): G = X^T X (cuBLAS, bf16 in, fp32 out, tensor
+ * cores), eigen-decomposition in fp64 (cuSOLVER dsyevd), A = X V_r (our fp32 CUDA-core kernel).  Each
+ * singular vector's largest-magnitude component is made positive (deterministic factors).
+ * Dims used: batch, n_kv_heads, head_dim (multiple of 32), ctx_len, rank (multiple of 16,
+ * 16 <= r <= min(256, s, h_kv*d)); h_kv*d <= 4096.  Prefill-time ("linear cost"), not the
+ * decode hot path; creates one cuBLAS and one cuSOLVER handle per process on first use.
+ * K_pre  device bf16 [b][h_kv][s][d]  (Alg 1 input K)
+ * A      device bf16 [b][s][r]        (out)
+ * B      device bf16 [b][h_kv][r][d]  (out)
+ * sigma  nullable device fp32 [b][r]  (out) singular values sigma_1 >= ... >= sigma_r */
+SKV_API skv_status shadowkv_factorize(const skv_dims *dims, const uint16_t *K_pre, uint16_t *A, uint16_t *B,
+                              float *sigma, void *workspace, void *stream);
+
 /* Thread-local description of the last non-OK status ("" if none). */
 SKV_API const char *shadowkv_last_error(void);
 

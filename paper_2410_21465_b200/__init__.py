@@ -4,4 +4,4 @@ The hot path lives in ``lib/libshadowkv.so`` (CUDA C, C ABI in include/shadowkv.
 ``binding`` is a ctypes marshalling layer and ``state`` allocates the per-layer tensors.
 """
 from . import binding  # noqa: F401
-from .state import LayerState, RopeTable, Shape, alloc_workspace  # noqa: F401
+from .state import LayerState, RopeTable, Shape, alloc_workspace, factorize  # noqa: F401

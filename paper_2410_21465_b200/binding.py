@@ -18,7 +18,8 @@ SKV_OK, SKV_EINVAL, SKV_EUNSUPPORTED, SKV_ECUDA, SKV_ESTATE = range(5)
 STATUS_NAMES = {0: "SKV_OK", 1: "SKV_EINVAL", 2: "SKV_EUNSUPPORTED", 3: "SKV_ECUDA", 4: "SKV_ESTATE"}
 EXPORTED = ["shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step", "shadowkv_decode_step_dev",
             "shadowkv_last_error", "shadowkv_abi_version", "shadowkv_last_launch_count",
-            "shadowkv_profile_begin", "shadowkv_profile_end", "shadowkv_trace_buffer"]
+            "shadowkv_profile_begin", "shadowkv_profile_end", "shadowkv_trace_buffer",
+            "shadowkv_factorize_workspace_bytes", "shadowkv_factorize"]
 KERNEL_NAMES = ["score", "select", "sparse_attn", "reserved", "combine"]
 
 
@@ -69,6 +70,11 @@ def load(path: str = LIB_PATH):
     lib.shadowkv_decode_step_dev.argtypes = [P(SkvDims), P(SkvRope), P(SkvLayer), ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.shadowkv_factorize_workspace_bytes.restype = ctypes.c_size_t
+    lib.shadowkv_factorize_workspace_bytes.argtypes = [P(SkvDims)]
+    lib.shadowkv_factorize.restype = ctypes.c_int
+    lib.shadowkv_factorize.argtypes = [P(SkvDims), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     lib.shadowkv_last_error.restype = ctypes.c_char_p
     lib.shadowkv_last_error.argtypes = []
     lib.shadowkv_abi_version.restype = ctypes.c_int32
@@ -167,3 +173,15 @@ def shadowkv_profile_end():
 def shadowkv_trace_buffer(buf):
     """Enable (device tensor of >= 4*4096*16 int64) or disable (None) the kernels' globaltimer stamps."""
     _check(load().shadowkv_trace_buffer(_ptr(buf)))
+
+
+def shadowkv_factorize_workspace_bytes(dims: SkvDims) -> int:
+    n = load().shadowkv_factorize_workspace_bytes(ctypes.byref(dims))
+    if n == 0:
+        raise ShadowKVError(SKV_EINVAL, load().shadowkv_last_error().decode())
+    return n
+
+
+def shadowkv_factorize(dims: SkvDims, K_pre, A, B, sigma=None, workspace=None, stream=None):
+    _check(load().shadowkv_factorize(ctypes.byref(dims), _ptr(K_pre), _ptr(A), _ptr(B), _ptr(sigma),
+                                     _ptr(workspace), _stream_ptr(stream)))

@@ -10,11 +10,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libshadowkv.so")
-SOURCES = ["abi.cu", "build.cu", "decode.cu", "score_tc.cu"]
+SOURCES = ["abi.cu", "build.cu", "decode.cu", "score_tc.cu", "factorize.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
-         "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-Xptxas", "-v"]
+         "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-Xptxas", "-v",
+         "-L/usr/local/cuda/lib64", "-lcublas", "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def _stale() -> bool:

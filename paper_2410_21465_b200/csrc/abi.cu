@@ -219,6 +219,52 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
   return SKV_OK;
 }
 
+// Alg 1 "A, B <- SVD(K)": dims used are batch, n_kv_heads, head_dim, ctx_len, rank.
+static skv_status check_factorize_dims(const skv_dims* d, int* D) {
+  if (!d) return fail(SKV_EINVAL, "dims is NULL");
+  if (d->batch < 1 || d->n_kv_heads < 1 || d->head_dim < 1 || d->ctx_len < 1)
+    return fail(SKV_EINVAL, "batch, n_kv_heads, head_dim and ctx_len must be >= 1");
+  if (d->head_dim % 32) return fail(SKV_EUNSUPPORTED, "head_dim %d not a multiple of 32", d->head_dim);
+  const long long Dl = (long long)d->n_kv_heads * d->head_dim;
+  if (Dl > 4096) return fail(SKV_EUNSUPPORTED, "n_kv_heads * head_dim = %lld > 4096", Dl);
+  if (d->rank < 16 || d->rank > 256 || d->rank % 16)
+    return fail(SKV_EINVAL, "rank %d must be a multiple of 16 in [16, 256]", d->rank);
+  if (d->rank > Dl || d->rank > d->ctx_len)
+    return fail(SKV_EINVAL, "rank %d exceeds min(ctx_len, n_kv_heads * head_dim)", d->rank);
+  *D = (int)Dl;
+  return SKV_OK;
+}
+
+size_t shadowkv_factorize_workspace_bytes(const skv_dims* dims) {
+  int D = 0;
+  if (check_factorize_dims(dims, &D) != SKV_OK) return 0;
+  return skv::factorize_ws_bytes(D, dims->rank, nullptr, nullptr);
+}
+
+skv_status shadowkv_factorize(const skv_dims* dims, const uint16_t* K_pre, uint16_t* A, uint16_t* B, float* sigma,
+                              void* workspace, void* stream) {
+  int D = 0;
+  skv_status st;
+  if ((st = check_factorize_dims(dims, &D)) != SKV_OK) return st;
+  if (!K_pre || !A || !B) return fail(SKV_EINVAL, "K_pre, A and B must be non-NULL");
+  if (!aligned16(K_pre) || !aligned16(A) || !aligned16(B) || (sigma && !aligned16(sigma)))
+    return fail(SKV_EINVAL, "K_pre/A/B/sigma must be 16-byte aligned");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
+  skv::FactorizeWs ws;
+  skv::factorize_ws_bytes(D, dims->rank, &ws, static_cast<char*>(workspace));
+  int launches = 0;
+  skv::FactorizeResult r = skv::launch_factorize(dims->batch, dims->n_kv_heads, dims->head_dim, dims->ctx_len,
+                                                 dims->rank, K_pre, A, B, sigma, ws,
+                                                 static_cast<cudaStream_t>(stream), &launches);
+  if (r.err != cudaSuccess)
+    return fail(SKV_ECUDA, "factorize (%s%s%d): %s", r.what ? r.what : "?", r.unused ? ", lwork " : "", r.unused,
+                cudaGetErrorString(r.err));
+  g_launches = launches;
+  g_err.clear();
+  return SKV_OK;
+}
+
 static skv_status decode_impl(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
                               const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                               int32_t step, const int32_t* step_dev, uint16_t* out, int32_t* sel_ids,

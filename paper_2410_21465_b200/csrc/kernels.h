@@ -101,4 +101,25 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
                           int* launches, Profiler* prof);
 size_t decode_ws_total_bytes(const Dims& D);   // every sub-batch split's workspace fits
 
+// factorize.cu: Alg 1 "A, B <- SVD(K)" through the D x D Gram matrix (NEXT-2)
+constexpr size_t kFactorizeBlasWs = (size_t)32 << 20;   // cuBLAS workspace carved from ours
+struct FactorizeWs {
+  float* G;          // [D][D] fp32 Gram (column-major)
+  double* Gd;        // [D][D] fp64, overwritten by the eigenvectors
+  double* lam;       // [D] eigenvalues, ascending
+  float* W;          // [D][r] top-r right singular vectors
+  int* info;
+  void* blas_ws;
+  double* work;      // dsyevd work
+  size_t lwork;      // doubles
+};
+struct FactorizeResult {
+  cudaError_t err;
+  int unused;
+  const char* what;  // failing step
+};
+size_t factorize_ws_bytes(int D, int r, FactorizeWs* ws, char* base);
+FactorizeResult launch_factorize(int b, int hk, int d, int s, int r, const uint16_t* K, uint16_t* A, uint16_t* B,
+                                 float* sigma, const FactorizeWs& ws, cudaStream_t st, int* launches);
+
 }  // namespace skv

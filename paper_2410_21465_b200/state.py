@@ -118,3 +118,17 @@ class RopeTable:
         self.inv_freq = torch.as_tensor(inv_freq, dtype=torch.float32).to(device).contiguous()
         self.rotary_dim, self.interleaved = int(rotary_dim), bool(interleaved)
         self.struct = bd.rope_struct(self.rotary_dim, self.interleaved, self.inv_freq)
+
+
+def factorize(K_pre: torch.Tensor, rank: int, stream=None):
+    """Alg 1 "A, B <- SVD(K)" on the GPU through shadowkv_factorize.
+    K_pre: device bf16 [b][h_kv][s][d] -> (A bf16 [b][s][r], B bf16 [b][h_kv][r][d], sigma fp32 [b][r])."""
+    b, hk, s, d = K_pre.shape
+    dims = bd.dims_struct(b, hk, hk, d, s, rank, 8, 0, 1, 0, 1)
+    n = bd.shadowkv_factorize_workspace_bytes(dims)
+    ws = torch.empty(n + 256, dtype=torch.uint8, device=K_pre.device)
+    A = torch.empty(b, s, rank, dtype=torch.bfloat16, device=K_pre.device)
+    B = torch.empty(b, hk, rank, d, dtype=torch.bfloat16, device=K_pre.device)
+    sigma = torch.empty(b, rank, dtype=torch.float32, device=K_pre.device)
+    bd.shadowkv_factorize(dims, K_pre.contiguous(), A, B, sigma, ws_ptr(ws), stream)
+    return A, B, sigma

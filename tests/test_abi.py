@@ -116,3 +116,20 @@ def test_ctypes_layer_struct_matches_header(tmp_path):
 def test_python_binding_raises_on_error(lib):
     with pytest.raises(bd.ShadowKVError, match="SKV_EINVAL"):
         bd.shadowkv_workspace_bytes(_dims(budget=10_000))
+
+
+def test_factorize_argument_errors(lib):
+    """shadowkv_factorize validates before any CUDA call (S:46 rank range)."""
+    ok = bd.dims_struct(1, 8, 8, 128, 4096, 160, 8, 0, 1, 0, 1)
+    assert bd.shadowkv_factorize_workspace_bytes(ok) > 1024 * 1024 * 8 * 2   # G fp32 + fp64 at D = 1024
+    for kw, status in [(dict(rank=8), bd.SKV_EINVAL), (dict(rank=170), bd.SKV_EINVAL),
+                       (dict(n_kv_heads=64), bd.SKV_EUNSUPPORTED), (dict(ctx_len=100), bd.SKV_EINVAL),
+                       (dict(head_dim=100), bd.SKV_EUNSUPPORTED)]:
+        args = dict(batch=1, n_q_heads=8, n_kv_heads=8, head_dim=128, ctx_len=4096, rank=160, chunk=8,
+                    n_outlier=0, budget=1, window_ctx=0, window_cap=1)
+        args.update(kw)
+        d = bd.SkvDims(**args)
+        assert lib.shadowkv_factorize_workspace_bytes(ctypes.byref(d)) == 0
+        assert lib.shadowkv_factorize(ctypes.byref(d), 16, 16, 16, None, 256, None) == status
+    assert lib.shadowkv_factorize(ctypes.byref(ok), 0, 16, 16, None, 256, None) == bd.SKV_EINVAL
+    assert lib.shadowkv_factorize(ctypes.byref(ok), 16, 16, 16, None, 272, None) == bd.SKV_EINVAL

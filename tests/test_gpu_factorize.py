@@ -1,0 +1,89 @@
+"""GPU factorisation (Alg 1 "A, B <- SVD(K)") through the C ABI vs the oracle.
+
+The factor split is unique only up to signs, so the checks are on what is unique:
+* singular values sigma_1..sigma_r vs the oracle's fp64 LAPACK SVD (relative 1e-3);
+* rebuilt keys A.B (bf16 factors widened) vs the oracle's rank-r truncation, per-row L2 relative
+  <= 1e-2 (north_star's key tolerance, R23) -- for keys of exact rank <= r this is the keys themselves;
+* the GPU truncation error stays within 1 % (+ bf16 storage slack) of the Eckart-Young optimum;
+* A^T A ~ diag(sigma^2) (A = U_r Sigma_r).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import shadowkv_oracle as O
+from tests.parity import KEY_REL_TOL, f64
+
+pytestmark = pytest.mark.gpu
+
+
+def _keys(seed, b, hk, s, d, true_rank, noise):
+    """Pre-RoPE keys: AR(1) rank-`true_rank` factors (synth recipe) + isotropic noise, bf16."""
+    cfg = synth.CONFIGS["c1"].replace(batch=b, n_kv_heads=hk, n_q_heads=hk, head_dim=d, ctx_len=s, rank=true_rank)
+    L = synth.gen_layer(cfg, seed)
+    K = torch.einsum("btr,bhrd->bhtd", L["A"].float(), L["B"].float())
+    if noise:
+        g = torch.Generator().manual_seed(seed + 1)
+        K = K + noise * torch.randn(K.shape, generator=g)
+    return K.to(torch.bfloat16)
+
+
+CASES = {
+    "llama_exact_rank160": dict(b=1, hk=8, s=4096, d=128, true_rank=160, noise=0.0, r=160),
+    "llama_noisy_tail": dict(b=1, hk=8, s=4096, d=128, true_rank=200, noise=0.02, r=160),
+    "batch2_glm_ragged": dict(b=2, hk=2, s=1000, d=128, true_rank=48, noise=0.05, r=64),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_factorize_parity(name):
+    c = CASES[name]
+    K = _keys(3, c["b"], c["hk"], c["s"], c["d"], c["true_rank"], c["noise"])
+    from paper_2410_21465_b200 import factorize
+    A, B, sig = factorize(K.cuda(), c["r"])
+    torch.cuda.synchronize()
+    K64 = f64(K)
+    oA, oB, osig = O.factorize(K64, c["r"])
+    gA, gB, gsig = f64(A), f64(B), f64(sig)
+    r = c["r"]
+    for bi in range(c["b"]):
+        np.testing.assert_allclose(gsig[bi], osig[bi, :r], rtol=1e-3, atol=1e-3 * osig[bi, 0])
+    g_rec = np.einsum("btr,bhrd->bhtd", gA, gB)
+    o_rec = np.einsum("btr,bhrd->bhtd", oA, oB)
+    rel = np.linalg.norm(g_rec - o_rec, axis=-1) / np.maximum(np.linalg.norm(o_rec, axis=-1), 1e-6)
+    assert rel.max() <= KEY_REL_TOL, f"rebuilt keys: max per-row relative error {rel.max():.3g}"
+    for bi in range(c["b"]):
+        opt = math.sqrt((osig[bi, r:] ** 2).sum())
+        err = np.linalg.norm(g_rec[bi] - K64[bi])
+        slack = 2 ** -8 * np.linalg.norm(K64[bi])                # bf16 storage of A and B
+        assert err <= 1.01 * opt + slack, f"truncation error {err:.4g} vs Eckart-Young {opt:.4g}"
+        AtA = gA[bi].T @ gA[bi]
+        off = AtA - np.diag(np.diag(AtA))
+        assert np.abs(off).max() <= 2e-2 * gsig[bi, 0] ** 2
+        np.testing.assert_allclose(np.sqrt(np.diag(AtA)), gsig[bi], rtol=1e-2)
+
+
+def test_factorize_then_decode_matches_oracle():
+    """Prefill fully on the GPU: factorize -> build_cache (keys = RoPE(A.B)) -> decode_step, against the
+    oracle running build + decode on the same (GPU-produced) factors."""
+    from paper_2410_21465_b200 import factorize
+    from tests.parity import Problem, check_decode, outliers_valid
+    cfg = synth.CONFIGS["c1"].replace(ctx_len=2048, budget=16)
+    P = Problem(cfg, seed=4, steps=2)
+    K = torch.einsum("btr,bhrd->bhtd", P.inputs["A"].float(), P.inputs["B"].float()).to(torch.bfloat16)
+    A, B, _ = factorize(K.cuda(), cfg.rank)
+    P.st.A.copy_(A); P.st.B.copy_(B)
+    P.A64, P.B64 = f64(A), f64(B)
+    P.gpu_build()
+    ost = P.oracle_build()
+    gids = P.st.outlier_ids.cpu().numpy()
+    for h in range(cfg.n_kv_heads):
+        assert outliers_valid(gids[0, h], ost.mincos[0, h], cfg.n_outlier)
+    P.load_state_from_oracle(ost)
+    si = P.step_inputs(0)
+    gout, gsel, gkeys = P.gpu_decode(0, si)
+    oout, osel, oz, okeys, _ = P.oracle_decode(ost, 0, si)
+    check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
