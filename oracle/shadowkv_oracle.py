@@ -26,7 +26,7 @@ __all__ = [
     "bf16_round", "identity_store", "partition", "rope", "chunk_means", "chunk_min_cos",
     "smallest_o", "build", "BuildState", "landmark_scores", "normalise_group_max",
     "arg_topk", "rebuild_keys", "decode_step", "dense_attention", "softmax_attention",
-    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits", "factorize",
+    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits", "factorize", "normalise_sum_group_max",
 ]
 
 
@@ -195,6 +195,21 @@ def normalise_group_max(logits, mask):
     return np.where(mask, z, -np.inf)
 
 
+def normalise_sum_group_max(logits, mask):
+    """Alg 2 with s_q >= 1 query tokens (P:169-172): logits [g][s_q][n_c];
+    S = Softmax(P/sqrt d) per (q head, query token) over the landmarks, S1 = sum over s_q ("dim=-2"),
+    S2 = max over the KV group.  Returns z = log S2 (masked -inf), computed literally in the
+    probability domain (fp64): for s_q = 1 it equals normalise_group_max."""
+    lg = np.where(mask[None, None, :], logits, -np.inf)
+    mx = lg.max(axis=2, keepdims=True)
+    S = np.exp(lg - mx)
+    S = S / S.sum(axis=2, keepdims=True)
+    S1 = S.sum(axis=1)
+    S2 = S1.max(axis=0)
+    with np.errstate(divide="ignore"):
+        return np.where(mask, np.log(S2), -np.inf)
+
+
 def arg_topk(z, k: int):
     """Alg 2 "I <- ArgTopK(S2, k)": k largest z, ties -> lower index (R12), returned ascending."""
     order = np.lexsort((np.arange(len(z)), -z))
@@ -217,9 +232,16 @@ def decode_step(state: BuildState, A, B, V, q, k_new, v_new, step, k, inv_freq, 
                 interleaved, c, store=bf16_round):
     """One decode step of Alg 2 + sparse attention (R17, R18).
 
-    state is NOT modified; returns (out [b][h_q][d], sel [b][h_kv][k], z [b][h_kv][n_c],
-    rebuilt keys [b][h_kv][k*c][d] (unrounded), new_state with the window slot written).
+    q [b][h_q][d] (s_q = 1) or [b][h_q][s_q][d] (Alg 2's Q, NEXT-3; k_new, v_new then
+    [b][h_kv][s_q][d]).  Query token i sits at position s + step + i and attends causally to the
+    new tokens 0..i (R28); the selection is shared by the s_q tokens (S1 = sum over s_q).
+    state is NOT modified; returns (out [b][h_q][d] or [b][h_q][s_q][d], sel [b][h_kv][k],
+    z [b][h_kv][n_c], rebuilt keys [b][h_kv][k*c][d] (unrounded), new_state with the window
+    slots written).
     """
+    if np.ndim(q) == 4:
+        return _decode_step_multi(state, A, B, V, q, k_new, v_new, step, k, inv_freq, rotary_dim,
+                                  interleaved, c, store)
     A = np.asarray(A, np.float64); B = np.asarray(B, np.float64); V = np.asarray(V, np.float64)
     q = np.asarray(q, np.float64); k_new = np.asarray(k_new, np.float64)
     v_new = np.asarray(v_new, np.float64)
@@ -260,6 +282,51 @@ def decode_step(state: BuildState, A, B, V, q, k_new, v_new, step, k, inv_freq, 
             keys, vals = keys[order], vals[order]
             for j in range(g):
                 out[bi, h * g + j] = softmax_attention(qg[j], keys, vals)
+    return out, sel, Z, Kt, st
+
+
+def _decode_step_multi(state, A, B, V, q, k_new, v_new, step, k, inv_freq, rotary_dim, interleaved, c,
+                       store):
+    """decode_step for s_q >= 1 query tokens (Alg 2 with Q in R^{b x h_q x s_q x d})."""
+    A = np.asarray(A, np.float64); B = np.asarray(B, np.float64); V = np.asarray(V, np.float64)
+    q = np.asarray(q, np.float64); k_new = np.asarray(k_new, np.float64)
+    v_new = np.asarray(v_new, np.float64)
+    st = state.copy()
+    nb, s, _ = A.shape
+    hk, d = B.shape[1], B.shape[3]
+    hq_n, sq = q.shape[1], q.shape[2]
+    g = hq_n // hk                         # R2
+    n_c, w_eff = st.n_c, st.w_eff
+    slot0 = w_eff + step
+    assert slot0 + sq <= st.K_win.shape[2]
+    for i in range(sq):                    # the s_q current tokens join the window (P:164, R18)
+        st.K_win[:, :, slot0 + i] = k_new[:, :, i]
+        st.V_win[:, :, slot0 + i] = v_new[:, :, i]
+    out = np.zeros((nb, hq_n, sq, d)); sel = np.zeros((nb, hk, k), np.int64)
+    Z = np.zeros((nb, hk, n_c)); Kt = np.zeros((nb, hk, k * c, d))
+    for bi in range(nb):
+        for h in range(hk):
+            mask = np.ones(n_c, bool)
+            mask[st.outlier_ids[bi, h]] = False
+            qg = q[bi, h * g:(h + 1) * g]                               # [g][s_q][d]
+            logits = np.stack([landmark_scores(qg[:, i], st.landmarks[bi, h], d) for i in range(sq)], axis=1)
+            z = normalise_sum_group_max(logits, mask)
+            ids = arg_topk(z, k)
+            tok = (ids[:, None] * c + np.arange(c)[None, :]).reshape(-1)
+            kt = rebuild_keys(A[bi], B[bi, h], tok, inv_freq, rotary_dim, interleaved)
+            vt = V[bi, h, tok]
+            Z[bi, h] = z; sel[bi, h] = ids; Kt[bi, h] = kt
+            otok = (st.outlier_ids[bi, h][:, None] * c + np.arange(c)[None, :]).reshape(-1)
+            for i in range(sq):
+                last = slot0 + i                                        # causal among the new tokens
+                wpos = np.array([n_c * c + j if j < w_eff else s + (j - w_eff) for j in range(last + 1)],
+                                dtype=np.int64)
+                pos = np.concatenate([otok, tok, wpos])
+                keys = np.concatenate([st.K_out[bi, h], kt, st.K_win[bi, h, :last + 1]])
+                vals = np.concatenate([st.V_out[bi, h], vt, st.V_win[bi, h, :last + 1]])
+                order = np.argsort(pos, kind="stable")
+                for j in range(g):
+                    out[bi, h * g + j, i] = softmax_attention(qg[j, i], keys[order], vals[order])
     return out, sel, Z, Kt, st
 
 

@@ -349,3 +349,55 @@ def test_paper_operating_point_arithmetic():
     of = GOLD["outlier_fraction"]
     frac = of["o"] / O.partition(of["s"], of["c"], 16)[0]
     assert of["lo"] <= frac <= of["hi"]
+
+
+# ---------------------------------------------------------------- s_q > 1 (NEXT-3, Alg 2's Q[b][h_q][s_q][d])
+def test_multi_query_sum_hand_example():
+    ex = GOLD["multi_query_sum_example"]
+    lg = np.array(ex["logits"])
+    z = O.normalise_sum_group_max(lg, np.ones(lg.shape[-1], bool))
+    np.testing.assert_allclose(np.exp(z), ex["S1"], atol=1e-6)
+    assert O.arg_topk(z, 1)[0] == ex["top1"]
+
+
+def test_multi_query_reduces_to_single_query():
+    """s_q = 1: normalise_sum_group_max == normalise_group_max, and the 4-D decode == the 3-D decode."""
+    rng = np.random.default_rng(21)
+    lg = rng.normal(size=(3, 1, 40)) * 2
+    mask = rng.random(40) > 0.2
+    np.testing.assert_allclose(O.normalise_sum_group_max(lg, mask)[mask], O.normalise_group_max(lg[:, 0], mask)[mask],
+                               atol=1e-12)
+    s, hk, g, d, c, o, w = 160, 2, 2, 16, 8, 2, 8
+    A, B, V, inv, rot, rng = _small_problem(22, s=s, hk=hk, g=g, d=d, w=w)
+    n_c, w_eff = O.partition(s, c, w)
+    st = O.build(A, B, V, inv, d, False, c, o, w, w_eff + 2)
+    q = rng.normal(size=(1, hk * g, d)); kn = rng.normal(size=(1, hk, d)); vn = rng.normal(size=(1, hk, d))
+    o3, s3, z3, k3, _ = O.decode_step(st, A, B, V, q, kn, vn, 1, 5, inv, d, False, c)
+    o4, s4, z4, k4, _ = O.decode_step(st, A, B, V, q[:, :, None], kn[:, :, None], vn[:, :, None], 1, 5, inv, d,
+                                      False, c)
+    np.testing.assert_array_equal(s3, s4)
+    np.testing.assert_allclose(o4[:, :, 0], o3, atol=1e-12)
+    np.testing.assert_allclose(z4, z3, atol=1e-12)
+
+
+@pytest.mark.parametrize("sq", [2, 4])
+def test_multi_query_full_coverage_equals_causal_dense_attention(sq):
+    """k = n_L, exact keys: each of the s_q query tokens == dense attention over the context, the earlier
+    generated tokens and the new tokens up to and including itself (causal, R28)."""
+    s, hk, g, d, c, o, w = 150, 2, 2, 16, 8, 3, 6
+    A, B, V, inv, rot, rng = _small_problem(23, s=s, hk=hk, g=g, d=d, w=w)
+    n_c, w_eff = O.partition(s, c, w)
+    st = O.build(A, B, V, inv, d, False, c, o, w, w_eff + 2 * sq, store=O.identity_store)
+    keys_ctx = np.stack([_rope_complex(A[0] @ B[0, h], np.arange(s), inv, d, False) for h in range(hk)])
+    gk, gv = [], []
+    for call in range(2):
+        step = call * sq
+        q = rng.normal(size=(1, hk * g, sq, d)) * 2
+        kn = rng.normal(size=(1, hk, sq, d)); vn = rng.normal(size=(1, hk, sq, d))
+        out, sel, z, kt, st = O.decode_step(st, A, B, V, q, kn, vn, step, n_c - o, inv, d, False, c,
+                                            store=O.identity_store)
+        for i in range(sq):
+            gk.append(kn[0, :, i]); gv.append(vn[0, :, i])
+            keys = np.concatenate([keys_ctx, np.stack(gk, axis=1)], axis=1)
+            vals = np.concatenate([V[0], np.stack(gv, axis=1)], axis=1)
+            np.testing.assert_allclose(out[0, :, i], O.dense_attention(q[0, :, i], keys, vals), atol=1e-12)
