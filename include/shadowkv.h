@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SHADOWKV_ABI_VERSION 2
+#define SHADOWKV_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define SKV_API __attribute__((visibility("default")))
@@ -66,7 +66,12 @@ typedef struct {
   int32_t n_outlier;    /* o; 0 <= o < n_c                                              */
   int32_t budget;       /* k selected chunks per KV head; 1 <= k <= n_L           */
   int32_t window_ctx;   /* w; context tail kept exact on the GPU (R8)                           */
-  int32_t window_cap;   /* ring capacity in tokens per KV head; >= w_eff + (steps you will run)  */
+  int32_t window_cap;   /* ring capacity in tokens per KV head; >= w_eff + (tokens you will decode) */
+  int32_t q_len;        /* s_q query tokens per decode call (Alg 2's Q in R^{b x h_q x s_q x d},
+                           P:164; e.g. speculative verification); 0 or 1 = one token.  The s_q
+                           tokens share one selection (S1 = sum over s_q of the softmax)
+                           and attend causally among themselves (R28).  Needs g * s_q in
+                           {1, 2, 4, 8, 16} (else SKV_EUNSUPPORTED).                          */
 } skv_dims;
 
 typedef struct {
@@ -141,12 +146,13 @@ SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *ro
  *       every selected chunk is written to this step's slot buffer (R26)
  *   a6  out_hq = softmax attention of q_hq over outlier tokens + K~/V~ + window slots
  *       [0, w_eff+step] (R17)
- * q      device bf16 [b][h_q][d], post-RoPE at position s+step (R16)
- * k_new  device bf16 [b][h_kv][d] post-RoPE;  v_new device bf16 [b][h_kv][d]
- * out    device bf16 [b][h_q][d]
+ * q      device bf16 [b][h_q][s_q][d], token i post-RoPE at position s+step+i (R16)
+ * k_new  device bf16 [b][h_kv][s_q][d] post-RoPE;  v_new device bf16 [b][h_kv][s_q][d]
+ *        (written to window slots w_eff+step .. w_eff+step+s_q-1; the next call's step is step+s_q)
+ * out    device bf16 [b][h_q][s_q][d]
  * sel_ids   nullable device int32 [b][h_kv][k]  -- parity hook for a3
  * dbg_keys  nullable device bf16 [b][h_kv][k*c][d] -- parity hook for a4 (rebuilt, post-RoPE)
- * Requires window_cap >= w_eff + step + 1 (SKV_EINVAL otherwise).
+ * Requires window_cap >= w_eff + step + s_q (SKV_EINVAL otherwise).
  * Streams: all work is ordered after earlier work on `stream`, and later work on `stream` is
  * ordered after all of it.  For batches of >= 32 requests the call pipelines request sub-batches:
  * it forks part of the work onto internal high-priority streams (event fork/join, capture-safe)

@@ -26,7 +26,7 @@ KERNEL_NAMES = ["score", "select", "sparse_attn", "reserved", "combine"]
 class SkvDims(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("batch", "n_q_heads", "n_kv_heads", "head_dim", "ctx_len", "rank", "chunk",
-                 "n_outlier", "budget", "window_ctx", "window_cap")]
+                 "n_outlier", "budget", "window_ctx", "window_cap", "q_len")]
 
 
 class SkvRope(ctypes.Structure):
@@ -109,9 +109,9 @@ def _stream_ptr(stream):
 
 
 def dims_struct(batch, n_q_heads, n_kv_heads, head_dim, ctx_len, rank, chunk, n_outlier, budget,
-                window_ctx, window_cap) -> SkvDims:
+                window_ctx, window_cap, q_len=1) -> SkvDims:
     return SkvDims(batch, n_q_heads, n_kv_heads, head_dim, ctx_len, rank, chunk, n_outlier, budget,
-                   window_ctx, window_cap)
+                   window_ctx, window_cap, q_len)
 
 
 def rope_struct(rotary_dim: int, interleaved: bool, inv_freq) -> SkvRope:

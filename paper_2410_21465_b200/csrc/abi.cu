@@ -35,11 +35,12 @@ skv_status check_dims(const skv_dims* d, skv::Dims* D) {
   if (d->batch < 1) return fail(SKV_EINVAL, "batch must be >= 1 (got %d)", d->batch);
   if (d->n_q_heads < 1 || d->n_kv_heads < 1) return fail(SKV_EINVAL, "head counts must be >= 1");
   if (d->n_q_heads % d->n_kv_heads) return fail(SKV_EINVAL, "n_q_heads %% n_kv_heads != 0 (GQA)");
-  const int g = d->n_q_heads / d->n_kv_heads;
+  const int sq = d->q_len <= 0 ? 1 : d->q_len;
+  const int g = d->n_q_heads / d->n_kv_heads * sq;       // query rows per KV head
   if (d->head_dim != 128) return fail(SKV_EUNSUPPORTED, "head_dim must be 128 (got %d)", d->head_dim);
   if (d->chunk != 8) return fail(SKV_EUNSUPPORTED, "chunk must be 8 (got %d)", d->chunk);
   if (g != 1 && g != 2 && g != 4 && g != 8 && g != 16)
-    return fail(SKV_EUNSUPPORTED, "GQA group %d not in {1,2,4,8,16}", g);
+    return fail(SKV_EUNSUPPORTED, "GQA group x q_len = %d not in {1,2,4,8,16}", g);
   if (d->rank < 16 || d->rank > 256) return fail(SKV_EINVAL, "rank %d out of range [16, 256]", d->rank);
   if (d->rank % 16) return fail(SKV_EUNSUPPORTED, "rank %d not a multiple of 16", d->rank);
   if (d->window_ctx < 0) return fail(SKV_EINVAL, "window_ctx must be >= 0");
@@ -55,8 +56,8 @@ skv_status check_dims(const skv_dims* d, skv::Dims* D) {
     return fail(SKV_EINVAL, "budget %d must satisfy 1 <= k <= n_L = %d", d->budget, n_c - d->n_outlier);
   if (d->window_cap < w_eff || d->window_cap < 1)
     return fail(SKV_EINVAL, "window_cap %d < w_eff %d", d->window_cap, w_eff);
-  *D = skv::Dims{d->batch, d->n_q_heads, d->n_kv_heads, g, d->head_dim, d->ctx_len, d->rank, d->chunk,
-                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff, 0, nullptr, 0};
+  *D = skv::Dims{d->batch, d->n_q_heads * sq, d->n_kv_heads, g, d->head_dim, d->ctx_len, d->rank, d->chunk,
+                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff, 0, nullptr, 0, sq};
   return SKV_OK;
 }
 
@@ -280,8 +281,9 @@ static skv_status decode_impl(const skv_dims* dims, const skv_rope* rope, const 
   if ((st = check_rope(rope, D.d, &R)) != SKV_OK) return st;
   if ((st = check_layer(layer, D, &Ly)) != SKV_OK) return st;
   if (step < 0) return fail(SKV_EINVAL, "step must be >= 0");
-  if (D.w_eff + step + 1 > D.wcap)
-    return fail(SKV_EINVAL, "window overflow: w_eff %d + step %d + 1 > window_cap %d", D.w_eff, step, D.wcap);
+  if (D.w_eff + step + D.sq > D.wcap)
+    return fail(SKV_EINVAL, "window overflow: w_eff %d + step %d + q_len %d > window_cap %d", D.w_eff, step, D.sq,
+                D.wcap);
   if (!q || !k_new || !v_new || !out) return fail(SKV_EINVAL, "q, k_new, v_new and out must be non-NULL");
   if (!aligned16(q) || !aligned16(k_new) || !aligned16(v_new) || !aligned16(out) ||
       (sel_ids && !aligned16(sel_ids)) || (dbg_keys && !aligned16(dbg_keys)))

@@ -127,10 +127,11 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
   pdl_trigger();                                       // let the select grid become resident early
   // a7: append the current token's K, V to the window (R18)
   const int stp = cur_step(D, step);
-  for (int idx = blockIdx.x * 256 + tid; idx < D.b * D.hk * 32; idx += gridDim.x * 256) {
-    const int bh = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;
-    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + stp) * kHeadDim + p * 8;
-    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bh * kHeadDim + p * 8;
+  for (int idx = blockIdx.x * 256 + tid; idx < D.b * D.hk * D.sq * 32; idx += gridDim.x * 256) {
+    const int bhi = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;    // (b, h, new token i)
+    const int bh = bhi / D.sq, i = bhi - bh * D.sq;
+    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + stp + i) * kHeadDim + p * 8;
+    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bhi * kHeadDim + p * 8;
     *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
   }
   if (tid == 0) {
@@ -305,6 +306,8 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   float zmax = -INFINITY;
 #pragma unroll
   for (int hq = 0; hq < G; ++hq) zmax = fmaxf(zmax, hm[hq] - lse[hq]);
+  const int sq = D.sq;
+  if (sq > 1) zmax += logf((float)sq);    // z = log sum_i S_i <= max_i log S_i + log s_q (an upper bound)
   trace(1, 2);
   // ---- z = max_g (l - lse) on the slice (R4, R5) + bucket histogram
   constexpr int U = G >= 8 ? 1 : 4;
@@ -320,8 +323,20 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT + tid;
       float zz = -INFINITY;
+      if (sq == 1) {
 #pragma unroll
-      for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lg[u][hq] - lse[hq]);
+        for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lg[u][hq] - lse[hq]);
+      } else {             // s_q query tokens per q head (rows hq*s_q + i): z = max_hq log sum_i S_{hq,i}
+        for (int r0 = 0; r0 < G; r0 += sq) {
+          float m = -INFINITY;
+          for (int i = 0; i < sq; ++i) m = fmaxf(m, lg[u][r0 + i] - lse[r0 + i]);
+          if (m > -INFINITY) {
+            float acc = 0.f;
+            for (int i = 0; i < sq; ++i) acc += expf(lg[u][r0 + i] - lse[r0 + i] - m);
+            zz = fmaxf(zz, m + logf(acc));
+          }
+        }
+      }
       if (j < len) {
         z[j] = zz;
         // the catch-all bucket 255 is never counted: if bins 0..254 hold fewer than k, B stays 255
@@ -633,7 +648,8 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane & 15;
   const int d = tid & 127, hh = tid >> 7;                      // PV / merge ownership: dim, head parity
   const int BH = D.b * D.hk;
-  const int T_out = D.o * kChunk, T_win = D.w_eff + cur_step(D, step) + 1;
+  const int stp0 = cur_step(D, step);
+  const int T_out = D.o * kChunk, T_win = D.w_eff + stp0 + D.sq;   // window incl. the s_q new tokens
   int u = blockIdx.x, kind, bh, ui;
   if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
   else {
@@ -841,7 +857,9 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       reduce_scatter16<16>(pv, sub);
       if (sub < 4 * HC) {
         const int i = sub / HC, hq = h0 + sub % HC, row = ty + 16 * i;
-        P[hq * kUnitTok + row] = row < ntok ? pv[0] * scale : -INFINITY;
+        // window unit: query row hq (token i = hq % s_q) sees new tokens 0..i only (causal, R28)
+        const bool vis = row < ntok && (kind != 2 || ui * kUnitTok + row < T_win - D.sq + 1 + hq % D.sq);
+        P[hq * kUnitTok + row] = vis ? pv[0] * scale : -INFINITY;
       }
     }
   }
@@ -850,7 +868,8 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   for (int hq = warp; hq < G; hq += 8) {
     float x0 = P[hq * kUnitTok + lane], x1 = P[hq * kUnitTok + lane + 32];
     const float m = warp_max(fmaxf(x0, x1));
-    const float e0 = expf(x0 - m), e1 = expf(x1 - m);
+    // (a row can be fully masked: a window unit past this query token's causal limit)
+    const float e0 = x0 > -INFINITY ? expf(x0 - m) : 0.f, e1 = x1 > -INFINITY ? expf(x1 - m) : 0.f;
     P[hq * kUnitTok + lane] = e0;
     P[hq * kUnitTok + lane + 32] = e1;
     const float l = warp_sum(e0 + e1);
@@ -1040,7 +1059,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     if (ev_sel && (e = cudaEventRecord(ev_sel, st))) return e;   // sub-batch pipelining: next chain may start
   }
   const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
-  const int n_win_u = (D.w_eff + (D.step_dev ? D.max_step : step) + 1 + kUnitTok - 1) / kUnitTok;
+  const int n_win_u = (D.w_eff + (D.step_dev ? D.max_step : step) + D.sq + kUnitTok - 1) / kUnitTok;
   const int n_split = n_sel_u + n_out_u + n_win_u;
   const int units = D.b * D.hk * n_split;
   // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score
@@ -1160,7 +1179,8 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
     decode_ws_bytes(Ds, &ws, ws_base + offs[i]);
     cudaStream_t si = i == 0 ? st : side[i - 1];
     if (i > 0 && (e = cudaStreamWaitEvent(si, ev_sel[i - 1], 0))) return e;
-    e = launch_decode_one(Ds, R, L, q + (size_t)r0 * hq * d, k_new + (size_t)r0 * hk * d, v_new + (size_t)r0 * hk * d,
+    e = launch_decode_one(Ds, R, L, q + (size_t)r0 * hq * d, k_new + (size_t)r0 * hk * D.sq * d,
+                          v_new + (size_t)r0 * hk * D.sq * d,
                           step, out + (size_t)r0 * hq * d, sel_ids ? sel_ids + (size_t)r0 * hk * D.k : nullptr,
                           dbg_keys ? dbg_keys + (size_t)r0 * hk * D.k * kChunk * d : nullptr, ws, si, launches,
                           nullptr, i + 1 < n ? ev_sel[i] : nullptr);

@@ -7,11 +7,12 @@
 namespace skv {
 
 struct Dims {          // validated, derived sizes
-  int b, hq, hk, g, d, s, r, c, o, k, w, wcap;
+  int b, hq, hk, g, d, s, r, c, o, k, w, wcap;   // hq, g: query ROWS (q heads x s_q query tokens)
   int n_c, w_eff;
   int trace_slot;      // tuning only: which [4][4096][16] block of the trace buffer this call stamps
   const int* step_dev; // graph-replayable decode: step read on the device (nullable), clamped to
   int max_step;        // [0, max_step]; the grid is sized for max_step
+  int sq;              // s_q query tokens per call (rows of one q head are consecutive: hq*s_q + i)
 };
 constexpr size_t kTraceSlot = (size_t)4 * 4096 * 16;
 

@@ -26,6 +26,7 @@ class Shape:
     budget: int
     window_ctx: int
     window_cap: int
+    q_len: int = 1          # s_q query tokens per decode call (Alg 2's Q[b][h_q][s_q][d])
 
     @property
     def n_c(self) -> int:          # grid chunks (window absorbs the ragged tail, DESIGN R8)
@@ -38,14 +39,15 @@ class Shape:
     def dims(self) -> bd.SkvDims:
         return bd.dims_struct(self.batch, self.n_q_heads, self.n_kv_heads, self.head_dim, self.ctx_len,
                               self.rank, self.chunk, self.n_outlier, self.budget, self.window_ctx,
-                              self.window_cap)
+                              self.window_cap, self.q_len)
 
     @classmethod
-    def from_config(cls, cfg, steps: int = 64, batch: int | None = None) -> "Shape":
+    def from_config(cls, cfg, steps: int = 64, batch: int | None = None, q_len: int = 1) -> "Shape":
+        """`steps` decode calls of `q_len` tokens each fit in the window."""
         s, w, c = cfg.ctx_len, cfg.window_ctx, cfg.chunk
         w_eff = s - ((s - w) // c) * c
         return cls(cfg.batch if batch is None else batch, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, s,
-                   cfg.rank, c, cfg.n_outlier, cfg.budget, w, w_eff + steps)
+                   cfg.rank, c, cfg.n_outlier, cfg.budget, w, w_eff + steps * q_len, q_len)
 
 
 def alloc_workspace(shape: Shape, device="cuda") -> torch.Tensor:

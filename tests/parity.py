@@ -56,12 +56,13 @@ class Problem:
     """Seeded synthetic inputs for one layer (synth), the GPU state and the oracle state."""
 
     def __init__(self, cfg: synth.Config, seed: int, steps: int = 4, K_rope: bool = False, device="cuda",
-                 value_cache: bool = False):
+                 value_cache: bool = False, q_len: int = 1):
         from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
         self.cfg, self.seed, self.steps = cfg, seed, steps
         self.inputs = synth.gen_layer(cfg, seed)
         self.inv, self.rot, self.il = synth.rope_table(cfg)
-        self.shape = Shape.from_config(cfg, steps=steps)
+        self.q_len = q_len
+        self.shape = Shape.from_config(cfg, steps=steps, q_len=q_len)
         self.st = LayerState(self.shape, device=device, value_cache=value_cache)
         self.st.A.copy_(self.inputs["A"]); self.st.B.copy_(self.inputs["B"])
         self.st.V_host.copy_(self.inputs["V"])
@@ -96,13 +97,18 @@ class Problem:
         self.st.V_win.copy_(torch.from_numpy(ost.V_win).to(bf))
 
     def step_inputs(self, step):
-        return synth.gen_step(self.cfg, self.seed, 0, step)
+        """One decode call's inputs; with q_len > 1 the tokens of steps step..step+q_len-1 stacked as
+        Alg 2's Q [b][h_q][s_q][d], K, V [b][h_kv][s_q][d]."""
+        if self.q_len == 1:
+            return synth.gen_step(self.cfg, self.seed, 0, step)
+        toks = [synth.gen_step(self.cfg, self.seed, 0, step + i) for i in range(self.q_len)]
+        return {n: torch.stack([t[n] for t in toks], dim=2) for n in ("q", "k_new", "v_new")}
 
     def gpu_decode(self, step, si, st=None):
         c, b = self.cfg, self.cfg.batch
         dev = "cuda"
         st = self.st if st is None else st
-        out = torch.empty(b, c.n_q_heads, c.head_dim, dtype=torch.bfloat16, device=dev)
+        out = torch.empty(si["q"].shape, dtype=torch.bfloat16, device=dev)
         sel = torch.empty(b, c.n_kv_heads, c.budget, dtype=torch.int32, device=dev)
         dbg = torch.empty(b, c.n_kv_heads, c.budget * c.chunk, c.head_dim, dtype=torch.bfloat16, device=dev)
         st.decode(self.rope.struct, si["q"].to(dev), si["k_new"].to(dev), si["v_new"].to(dev), step, out,

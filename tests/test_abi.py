@@ -27,7 +27,7 @@ def test_header_declares_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert bd.shadowkv_abi_version() == 2
+    assert bd.shadowkv_abi_version() == 3
 
 
 def _dims(**kw):
@@ -133,3 +133,19 @@ def test_factorize_argument_errors(lib):
         assert lib.shadowkv_factorize(ctypes.byref(d), 16, 16, 16, None, 256, None) == status
     assert lib.shadowkv_factorize(ctypes.byref(ok), 0, 16, 16, None, 256, None) == bd.SKV_EINVAL
     assert lib.shadowkv_factorize(ctypes.byref(ok), 16, 16, 16, None, 272, None) == bd.SKV_EINVAL
+
+
+def test_q_len_validation(lib):
+    """s_q query tokens (NEXT-3): g * s_q must be a compiled row count; the window must hold s_q new tokens."""
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(q_len=4))) > 0           # g 4 x 4 = 16 rows
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(q_len=3))) == 0           # 12 rows
+    assert "q_len" in lib.shadowkv_last_error().decode()
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(q_len=8))) == 0           # 32 rows
+    # more rows -> more logits workspace
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(q_len=2))) > lib.shadowkv_workspace_bytes(ctypes.byref(_dims()))
+    d = _dims(q_len=4, window_cap=16 + 4)
+    rope = bd.SkvRope(128, 0, 16)
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 3))
+    call = lambda step: lib.shadowkv_decode_step(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(layer), 16, 16, 16,
+                                                 step, 16, None, None, 256, None)
+    assert call(1) == bd.SKV_EINVAL and "q_len" in lib.shadowkv_last_error().decode()   # 16 + 1 + 4 > 20

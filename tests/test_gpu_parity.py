@@ -250,3 +250,21 @@ def test_decode_step_dev_and_graph_replay(name):
             g.replay()
             torch.cuda.synchronize()
             assert torch.equal(out_b, ref[s]), f"graph replay differs at step {s}"
+
+
+@pytest.mark.parametrize("name,q_len", [("c1", 2), ("c1", 4), ("g2_rank64", 8), ("g1_batch2", 2),
+                                        ("multi_tile_k", 4)])
+def test_decode_parity_multi_query(name, q_len):
+    """s_q = q_len query tokens per call (Alg 2's Q[b][h_q][s_q][d], NEXT-3): one shared selection from
+    S1 = sum over s_q, causal attention among the new tokens (R28); three calls in a row so the
+    window holds earlier multi-token appends."""
+    P = Problem(CASES[name], seed=6, steps=3, q_len=q_len)
+    ost = P.oracle_build()
+    P.load_state_from_oracle(ost)
+    for call in range(3):
+        step = call * q_len
+        si = P.step_inputs(step)
+        gout, gsel, gkeys = P.gpu_decode(step, si)
+        oout, osel, oz, okeys, ost = P.oracle_decode(ost, step, si)
+        assert gout.shape == oout.shape
+        check_decode(P.cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
