@@ -55,6 +55,9 @@ def parse():
                     help="value-cache leg (P:156, DESIGN R26/R27): comma list of query-drift correlations rho; "
                          "each runs the same step with a GPU value cache per layer and drifting queries and "
                          "reports the measured hit rate alpha ('' = skip)")
+    ap.add_argument("--q-len-leg", type=int, default=4,
+                    help="multi-query leg (NEXT-3, Alg 2's s_q): the same 32-layer step with s_q query tokens per "
+                         "call (speculative verification); 0 = skip")
     ap.add_argument("--layer-states", type=int, default=0,
                     help="distinct layer states cycled per step (default: the model's layer count)")
     return ap.parse_args()
@@ -337,6 +340,70 @@ def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_by
 
 
 # ------------------------------------------------------------------------------------------------
+def multi_query_leg(args, cfg, q_len, states, rope, seed, host_bytes, host_peak, dev):
+    """NEXT-3 (Alg 2 with Q in R^{b x h_q x s_q x d}): every decode call carries s_q query
+    tokens (e.g. draft tokens being verified) that share one selection and one value fetch.  Same
+    layer states and graph-timed 32-layer step as the main line; tokens/s counts s_q tokens per request
+    per step (all accepted: an upper bound for speculative decoding, the attention cost per call)."""
+    from paper_2410_21465_b200 import LayerState, Shape, alloc_workspace, shard
+    import copy
+    Lm, b = cfg.n_layers, cfg.batch
+    n_states = len(states)
+    steps, warm = args.steps, max(args.warmup, 3)
+    shape = Shape.from_config(cfg, steps=steps + warm + 1, q_len=q_len)
+    try:
+        ws = alloc_workspace(shape, device=dev)
+        layers = []
+        for l in range(n_states):
+            st = copy.copy(states[l])
+            st.shape = shape
+            # a window ring sized for this leg's s_q-token appends (context tail copied from the built state)
+            st.K_win = torch.zeros(b, cfg.n_kv_heads, shape.window_cap, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+            st.V_win = torch.zeros_like(st.K_win)
+            w_eff = shape.w_eff
+            st.K_win[:, :, :w_eff].copy_(states[l].K_win[:, :, :w_eff]); st.V_win[:, :, :w_eff].copy_(states[l].V_win[:, :, :w_eff])
+            layers.append(st)
+    except torch.OutOfMemoryError:
+        return {"skipped": "out of HBM", "q_len": q_len}
+    gen = torch.Generator(device=dev).manual_seed(seed + 31337)
+    q_g = (2.0 * torch.randn(Lm, b, cfg.n_q_heads, q_len, cfg.head_dim, device=dev, generator=gen)).to(torch.bfloat16)
+    k_g = torch.randn(Lm, b, cfg.n_kv_heads, q_len, cfg.head_dim, device=dev, generator=gen).to(torch.bfloat16)
+    v_g = torch.randn(k_g.shape, device=dev, generator=gen).to(torch.bfloat16)
+    out = torch.empty(Lm, b, cfg.n_q_heads, q_len, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+    qs = [(2.0 * torch.randn(q_g.shape, device=dev, generator=gen)).to(torch.bfloat16) for _ in range(4)]
+    step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+    max_step = (steps + warm) * q_len
+    cap = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        for l in range(Lm):
+            layers[l % n_states].decode_dev(rope.struct, q_g[l], k_g[l], v_g[l], step_dev, max_step, out[l], ws, stream=cap)
+        step_dev.add_(q_len)
+    step_dev.fill_(0)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    for i in range(warm):
+        q_g.copy_(qs[i % 4], non_blocking=True)
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        q_g.copy_(qs[i % 4], non_blocking=True)                  # fresh queries: fresh selections
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    value = shard.job_tokens_per_s(b * q_len, ms / 1e3, device=dev)
+    del g, layers, ws
+    torch.cuda.empty_cache()
+    return {"q_len": q_len, "value": value, "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
+            "step_frac_of_host_roofline": Lm * host_bytes / (host_peak * 1e9) / (ms * 1e-3),
+            "note": "s_q query tokens per request per call share one selection (S1 = sum over s_q, P:171) and one "
+                    "host value fetch; tokens/s counts all s_q tokens (every draft accepted)"}
+
+
+# ------------------------------------------------------------------------------------------------
 def run_ours(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -526,6 +593,10 @@ def run_ours(args, cfg):
         value_cache = [value_cache_leg(args, cfg, float(r), states, rope, ws, out, stream, seed, host_bytes, host_peak,
                                        n_total, dev) for r in args.vc_rho.split(",") if r.strip()]
 
+    multi_query = None
+    if args.q_len_leg and args.q_len_leg > 1:
+        multi_query = multi_query_leg(args, cfg, args.q_len_leg, states, rope, seed, host_bytes, host_peak, dev)
+
     breakdown = None
     if args.breakdown:
         bd.shadowkv_profile_begin(Lm * 5 * 20 + 8, 0x1F)
@@ -553,6 +624,8 @@ def run_ours(args, cfg):
             "setup_s": setup_s}
     if value_cache:
         line["value_cache"] = value_cache[0] if len(value_cache) == 1 else value_cache
+    if multi_query:
+        line["multi_query"] = multi_query
     if breakdown:
         line["kernel_breakdown_us"] = breakdown
     if world == 1 and not args.no_cpu_baseline:

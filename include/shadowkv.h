@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SHADOWKV_ABI_VERSION 3
+#define SHADOWKV_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define SKV_API __attribute__((visibility("default")))
@@ -72,6 +72,14 @@ typedef struct {
                            tokens share one selection (S1 = sum over s_q of the softmax)
                            and attend causally among themselves (R28).  Needs g * s_q in
                            {1, 2, 4, 8, 16} (else SKV_EUNSUPPORTED).                          */
+  /* Ragged batch: per-request context lengths s_b <= ctx_len.  Both NULL = every
+   * request has ctx_len tokens.  Otherwise ctx_len is the PADDED length every [..][s][..] layout
+   * (A, V_host, K_rope) and the landmark grid [..][n_c][..] (n_c of ctx_len) are strided by, and
+   * request b uses its own grid n_c(b) = floor((s_b - w)/c), window tail w_eff(b) = s_b - n_c(b)*c
+   * (R8 per request), decode positions s_b + step + i.  Each s_b must leave o + k chunks on its
+   * grid: s_b >= w + c*(o + k) (SKV_EINVAL otherwise).  window_cap must hold the largest w_eff(b). */
+  const int32_t *ctx_lens;      /* host int32 [b] (validated on every call)                       */
+  const int32_t *ctx_lens_dev;  /* device int32 [b], the same values (read by the kernels)        */
 } skv_dims;
 
 typedef struct {

@@ -26,7 +26,8 @@ KERNEL_NAMES = ["score", "select", "sparse_attn", "reserved", "combine"]
 class SkvDims(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
                 ("batch", "n_q_heads", "n_kv_heads", "head_dim", "ctx_len", "rank", "chunk",
-                 "n_outlier", "budget", "window_ctx", "window_cap", "q_len")]
+                 "n_outlier", "budget", "window_ctx", "window_cap", "q_len")] + \
+        [("ctx_lens", ctypes.c_void_p), ("ctx_lens_dev", ctypes.c_void_p)]
 
 
 class SkvRope(ctypes.Structure):
@@ -109,9 +110,11 @@ def _stream_ptr(stream):
 
 
 def dims_struct(batch, n_q_heads, n_kv_heads, head_dim, ctx_len, rank, chunk, n_outlier, budget,
-                window_ctx, window_cap, q_len=1) -> SkvDims:
+                window_ctx, window_cap, q_len=1, ctx_lens=None, ctx_lens_dev=None) -> SkvDims:
+    """ctx_lens: host int32 tensor / array [batch] of per-request lengths (ragged batch) with its device
+    mirror ctx_lens_dev; the caller keeps both alive while the struct is in use."""
     return SkvDims(batch, n_q_heads, n_kv_heads, head_dim, ctx_len, rank, chunk, n_outlier, budget,
-                   window_ctx, window_cap, q_len)
+                   window_ctx, window_cap, q_len, _ptr(ctx_lens), _ptr(ctx_lens_dev))
 
 
 def rope_struct(rotary_dim: int, interleaved: bool, inv_freq) -> SkvRope:

@@ -54,10 +54,27 @@ skv_status check_dims(const skv_dims* d, skv::Dims* D) {
     return fail(SKV_EINVAL, "n_outlier %d must satisfy 0 <= o < n_c = %d", d->n_outlier, n_c);
   if (d->budget < 1 || d->budget > n_c - d->n_outlier)
     return fail(SKV_EINVAL, "budget %d must satisfy 1 <= k <= n_L = %d", d->budget, n_c - d->n_outlier);
-  if (d->window_cap < w_eff || d->window_cap < 1)
-    return fail(SKV_EINVAL, "window_cap %d < w_eff %d", d->window_cap, w_eff);
+  int w_eff_max = w_eff;
+  if ((d->ctx_lens == nullptr) != (d->ctx_lens_dev == nullptr))
+    return fail(SKV_EINVAL, "ctx_lens and ctx_lens_dev: give both or neither");
+  if (d->ctx_lens) {                                     // ragged batch: every request's own grid (R8)
+    if (reinterpret_cast<uintptr_t>(d->ctx_lens_dev) & 3u) return fail(SKV_EINVAL, "ctx_lens_dev must be 4-byte aligned");
+    w_eff_max = 0;
+    const long long need = (long long)d->window_ctx + (long long)d->chunk * (d->n_outlier + d->budget);
+    for (int b = 0; b < d->batch; ++b) {
+      const int sb = d->ctx_lens[b];
+      if (sb > d->ctx_len || sb < need)
+        return fail(SKV_EINVAL, "ctx_lens[%d] = %d outside [w + c*(o + k) = %lld, ctx_len = %d]", b, sb, need,
+                    d->ctx_len);
+      const int ncb = (sb - d->window_ctx) / d->chunk;
+      w_eff_max = w_eff_max > sb - ncb * d->chunk ? w_eff_max : sb - ncb * d->chunk;
+    }
+  }
+  if (d->window_cap < w_eff_max || d->window_cap < 1)
+    return fail(SKV_EINVAL, "window_cap %d < w_eff %d", d->window_cap, w_eff_max);
   *D = skv::Dims{d->batch, d->n_q_heads * sq, d->n_kv_heads, g, d->head_dim, d->ctx_len, d->rank, d->chunk,
-                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff, 0, nullptr, 0, sq};
+                 d->n_outlier, d->budget, d->window_ctx, d->window_cap, n_c, w_eff_max, 0, nullptr, 0, sq,
+                 d->ctx_lens_dev};
   return SKV_OK;
 }
 

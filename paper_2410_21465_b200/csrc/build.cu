@@ -27,7 +27,8 @@ k_build_chunks(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ K_rope, fl
   float* Ks = reinterpret_cast<float*>(smem);
   int* tok = tile_tok_ptr(smem, D.r);
   const int j0 = tile * 16;
-  const int ntok = min(kTileTok, (D.n_c - j0) * kChunk);
+  const int ncb = req_nc(D, b);                         // this request's grid (ragged batch)
+  const int ntok = max(0, min(kTileTok, (ncb - j0) * kChunk));
   if (tid < kTileTok) tok[tid] = j0 * kChunk + tid;
   __syncthreads();
   produce_key_tile(Ly.A + (size_t)b * D.s * D.r, Ly.B + bh * D.r * kHeadDim,
@@ -38,6 +39,12 @@ k_build_chunks(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ K_rope, fl
   for (int cc = 0; cc < 2; ++cc) {
     const int jl = warp * 2 + cc, j = j0 + jl;
     if (j >= D.n_c) break;
+    if (j >= ncb) {                                     // padding past a shorter request's grid: never
+      const size_t row = bh * D.n_c + j;                // an outlier (-m = -inf), landmark row zero
+      if (lane == 0) { mincos[row] = INFINITY; negm[row] = -INFINITY; }
+      *reinterpret_cast<uint2*>(Ly.L + row * kHeadDim + lane * 4) = make_uint2(0u, 0u);
+      continue;
+    }
     float4 kv[kChunk];
     float4 C = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -78,13 +85,14 @@ k_build_outliers_window(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ K
   const size_t bh = (size_t)b * D.hk + h;
   float* Ks = reinterpret_cast<float*>(smem);
   int* tok = tile_tok_ptr(smem, D.r);
-  const int n_out = D.o * kChunk, total = n_out + D.w_eff;
+  const int n_out = D.o * kChunk, total = n_out + req_weff(D, b);   // this request's window tail
   const int i0 = tile * kTileTok;
   const int ntok = min(kTileTok, total - i0);
+  if (ntok <= 0) return;                                // (block-uniform) a shorter request's tail
   if (tid < kTileTok) {
     int i = i0 + tid, t = 0;
     if (i < n_out) t = Ly.outlier_ids[bh * D.o + (i >> 3)] * kChunk + (i & 7);
-    else if (i < total) t = D.n_c * kChunk + (i - n_out);
+    else if (i < total) t = req_nc(D, b) * kChunk + (i - n_out);
     tok[tid] = t;
   }
   __syncthreads();

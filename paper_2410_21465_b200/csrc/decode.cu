@@ -130,7 +130,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
   for (int idx = blockIdx.x * 256 + tid; idx < D.b * D.hk * D.sq * 32; idx += gridDim.x * 256) {
     const int bhi = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;    // (b, h, new token i)
     const int bh = bhi / D.sq, i = bhi - bh * D.sq;
-    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + stp + i) * kHeadDim + p * 8;
+    const size_t dst = ((size_t)bh * D.wcap + req_weff(D, bh / D.hk) + stp + i) * kHeadDim + p * 8;
     const uint16_t* src = (arr ? v_new : k_new) + (size_t)bhi * kHeadDim + p * 8;
     *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
   }
@@ -189,7 +189,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
       const int il = rl + sub / G, r = warp * 16 + il;
       if (il < 16 && r < rows) {
         const int j = j0 + r;
-        Pb[(sub % G) * kSTile + r] = ((obits[j >> 5] >> (j & 31)) & 1u) ? -INFINITY : dot * scale;
+        Pb[(sub % G) * kSTile + r] = (((obits[j >> 5] >> (j & 31)) & 1u) || j >= req_nc(D, b)) ? -INFINITY : dot * scale;
       }
     }
     __syncthreads();                                   // Pb complete; stage `st` free for reuse
@@ -649,7 +649,8 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   const int d = tid & 127, hh = tid >> 7;                      // PV / merge ownership: dim, head parity
   const int BH = D.b * D.hk;
   const int stp0 = cur_step(D, step);
-  const int T_out = D.o * kChunk, T_win = D.w_eff + stp0 + D.sq;   // window incl. the s_q new tokens
+  const int T_out = D.o * kChunk;
+  int T_win;                                           // this request's window incl. the s_q new tokens
   int u = blockIdx.x, kind, bh, ui;
   if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
   else {
@@ -659,6 +660,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     if (ui < n_out_u) kind = 1; else { kind = 2; ui -= n_out_u; }
   }
   const int b = bh / D.hk, h = bh - b * D.hk;
+  T_win = req_weff(D, b) + stp0 + D.sq;
   const int split = kind == 0 ? ui : (kind == 1 ? n_sel_u + ui : n_sel_u + n_out_u + ui);
   int32_t* slots = sel + (size_t)bh * D.k;                     // k_select's unordered selection (id + 1)
   const int nch = kind == 0 ? min(8, D.k - ui * 8) : 0;        // chunks of a selected-chunk unit (>= 1)
@@ -1159,7 +1161,8 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
   const size_t s = D.s, hk = D.hk, hq = D.hq, d = kHeadDim;
   for (int i = 0; i < n; ++i) {
     const int r0 = D.b * i / n, nb = D.b * (i + 1) / n - r0;
-    const Dims Ds = sub_dims(D, nb);
+    Dims Ds = sub_dims(D, nb);
+    if (D.lens) Ds.lens = D.lens + r0;
     Layer L = Ly;
     L.A = Ly.A + (size_t)r0 * s * D.r;
     L.B = Ly.B + (size_t)r0 * hk * D.r * d;

@@ -13,7 +13,17 @@ struct Dims {          // validated, derived sizes
   const int* step_dev; // graph-replayable decode: step read on the device (nullable), clamped to
   int max_step;        // [0, max_step]; the grid is sized for max_step
   int sq;              // s_q query tokens per call (rows of one q head are consecutive: hq*s_q + i)
+  const int* lens;     // ragged batch: device int32 [b] per-request context lengths (nullable = all s);
+                       // then s, n_c are the padded layout sizes and w_eff is the largest per-request w_eff
 };
+#ifdef __CUDACC__
+// per-request sizes of a ragged batch (R8 applied to each request's own length)
+__device__ __forceinline__ int req_s(const Dims& D, int b) { return D.lens ? __ldg(D.lens + b) : D.s; }
+__device__ __forceinline__ int req_nc(const Dims& D, int b) { return D.lens ? (__ldg(D.lens + b) - D.w) / D.c : D.n_c; }
+__device__ __forceinline__ int req_weff(const Dims& D, int b) {
+  return D.lens ? __ldg(D.lens + b) - req_nc(D, b) * D.c : D.w_eff;
+}
+#endif
 constexpr size_t kTraceSlot = (size_t)4 * 4096 * 16;
 
 struct Rope {

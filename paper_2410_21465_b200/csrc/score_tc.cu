@@ -187,7 +187,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   for (int idx = blockIdx.x * kTcThreads + tid; idx < D.b * D.hk * D.sq * 32; idx += gridDim.x * kTcThreads) {
     const int bhi = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;   // (b, h, new token i)
     const int bh = bhi / D.sq, i = bhi - bh * D.sq;
-    const size_t dst = ((size_t)bh * D.wcap + D.w_eff + stp + i) * kHeadDim + p * 8;
+    const size_t dst = ((size_t)bh * D.wcap + req_weff(D, bh / D.hk) + stp + i) * kHeadDim + p * 8;
     const uint16_t* src = (arr ? v_new : k_new) + (size_t)bhi * kHeadDim + p * 8;
     *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
   }
@@ -285,6 +285,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     if (grp == 1 && ntile > 1) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
     int cur_bh = t_begin / tiles_per_head;
     float* lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
+    int ncb = req_nc(D, bh / D.hk);                       // ragged batch: chunks past it are masked
     const int r = 32 * quad + lane;
     for (int i = grp; i < ntile; i += 2) {
       const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
@@ -293,6 +294,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         for (int e = cur_bh + 1; e < bh; ++e) flush(e);
         cur_bh = bh;
         lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
+        ncb = req_nc(D, bh / D.hk);
       }
       mbar_wait(&acc_full[buf], aph);
       tc_fence_after();
@@ -302,7 +304,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
       const int j = tile * kSTile + r;
-      const bool out = (obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u;
+      const bool out = ((obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u) || j >= ncb;
       if (warp == 0 && lane == 0 && i < 4) trace_tc_any(trace_buf, 8 + i);   // epilogue got tile i
       if (j < D.n_c) {
 #pragma unroll

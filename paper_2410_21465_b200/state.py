@@ -27,6 +27,7 @@ class Shape:
     window_ctx: int
     window_cap: int
     q_len: int = 1          # s_q query tokens per decode call (Alg 2's Q[b][h_q][s_q][d])
+    ctx_lens: tuple | None = None   # ragged batch: per-request context lengths (ctx_len = the padded length)
 
     @property
     def n_c(self) -> int:          # grid chunks (window absorbs the ragged tail, DESIGN R8)
@@ -36,18 +37,24 @@ class Shape:
     def w_eff(self) -> int:
         return self.ctx_len - self.n_c * self.chunk
 
-    def dims(self) -> bd.SkvDims:
+    def dims(self, lens_host=None, lens_dev=None) -> bd.SkvDims:
+        """skv_dims; a ragged shape needs its host / device length tensors (LayerState holds them)."""
         return bd.dims_struct(self.batch, self.n_q_heads, self.n_kv_heads, self.head_dim, self.ctx_len,
                               self.rank, self.chunk, self.n_outlier, self.budget, self.window_ctx,
-                              self.window_cap, self.q_len)
+                              self.window_cap, self.q_len, lens_host, lens_dev)
 
     @classmethod
-    def from_config(cls, cfg, steps: int = 64, batch: int | None = None, q_len: int = 1) -> "Shape":
-        """`steps` decode calls of `q_len` tokens each fit in the window."""
+    def from_config(cls, cfg, steps: int = 64, batch: int | None = None, q_len: int = 1,
+                    ctx_lens=None) -> "Shape":
+        """`steps` decode calls of `q_len` tokens each fit in the window.  ctx_lens: per-request
+        lengths of a ragged batch (cfg.ctx_len is then the padded length)."""
         s, w, c = cfg.ctx_len, cfg.window_ctx, cfg.chunk
         w_eff = s - ((s - w) // c) * c
+        if ctx_lens is not None:
+            ctx_lens = tuple(int(x) for x in ctx_lens)
+            w_eff = max(x - ((x - w) // c) * c for x in ctx_lens)
         return cls(cfg.batch if batch is None else batch, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, s,
-                   cfg.rank, c, cfg.n_outlier, cfg.budget, w, w_eff + steps * q_len, q_len)
+                   cfg.rank, c, cfg.n_outlier, cfg.budget, w, w_eff + steps * q_len, q_len, ctx_lens)
 
 
 def alloc_workspace(shape: Shape, device="cuda") -> torch.Tensor:
@@ -67,6 +74,10 @@ class LayerState:
                  value_cache: bool = False):
         self.shape = S = shape
         b, hk, d = S.batch, S.n_kv_heads, S.head_dim
+        self.lens_host = self.lens_dev = None
+        if S.ctx_lens is not None:                      # ragged batch: host + device length arrays
+            self.lens_host = torch.tensor(S.ctx_lens, dtype=torch.int32)
+            self.lens_dev = self.lens_host.to(device)
         bf = torch.bfloat16
         self.A = torch.empty(b, S.ctx_len, S.rank, dtype=bf, device=device)
         self.B = torch.empty(b, hk, S.rank, d, dtype=bf, device=device)
@@ -97,19 +108,22 @@ class LayerState:
         """-> int64 [b][h_kv][4] {generation, -, hits in the last step, hits in total} (synchronises)."""
         return None if self.vc_stats is None else self.vc_stats.cpu()
 
+    def dims(self) -> bd.SkvDims:
+        return self.shape.dims(self.lens_host, self.lens_dev)
+
     def build(self, rope: bd.SkvRope, workspace: torch.Tensor, K_rope: torch.Tensor | None = None, stream=None):
-        bd.shadowkv_build_cache(self.shape.dims(), rope, self.layer(), K_rope, ws_ptr(workspace), stream)
+        bd.shadowkv_build_cache(self.dims(), rope, self.layer(), K_rope, ws_ptr(workspace), stream)
 
     def decode(self, rope: bd.SkvRope, q, k_new, v_new, step: int, out, workspace, sel_ids=None,
                dbg_keys=None, stream=None):
-        bd.shadowkv_decode_step(self.shape.dims(), rope, self.layer(), q, k_new, v_new, step, out, sel_ids,
+        bd.shadowkv_decode_step(self.dims(), rope, self.layer(), q, k_new, v_new, step, out, sel_ids,
                                 dbg_keys, ws_ptr(workspace), stream)
 
 
     def decode_dev(self, rope: bd.SkvRope, q, k_new, v_new, step_dev, max_step: int, out, workspace,
                    sel_ids=None, dbg_keys=None, stream=None):
         """Graph-replayable decode: the step index is read on the device from step_dev (int32 tensor)."""
-        bd.shadowkv_decode_step_dev(self.shape.dims(), rope, self.layer(), q, k_new, v_new, step_dev, max_step, out,
+        bd.shadowkv_decode_step_dev(self.dims(), rope, self.layer(), q, k_new, v_new, step_dev, max_step, out,
                                     sel_ids, dbg_keys, ws_ptr(workspace), stream)
 
 

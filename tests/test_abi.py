@@ -27,7 +27,7 @@ def test_header_declares_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert bd.shadowkv_abi_version() == 3
+    assert bd.shadowkv_abi_version() == 4
 
 
 def _dims(**kw):
@@ -104,13 +104,13 @@ def test_ctypes_layer_struct_matches_header(tmp_path):
         pytest.skip("no C compiler")
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "shadowkv.h"\n'
-                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(skv_layer), offsetof(skv_layer, vc_values),'
-                   ' offsetof(skv_layer, vc_stats), sizeof(skv_dims), sizeof(skv_rope)); return 0;}\n')
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(skv_layer), offsetof(skv_layer, vc_values),'
+                   ' offsetof(skv_layer, vc_stats), sizeof(skv_dims), sizeof(skv_rope), offsetof(skv_dims, ctx_lens_dev)); return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run([cc, "-I", os.path.dirname(HDR), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert got == [ctypes.sizeof(bd.SkvLayer), bd.SkvLayer.vc_values.offset, bd.SkvLayer.vc_stats.offset,
-                   ctypes.sizeof(bd.SkvDims), ctypes.sizeof(bd.SkvRope)]
+                   ctypes.sizeof(bd.SkvDims), ctypes.sizeof(bd.SkvRope), bd.SkvDims.ctx_lens_dev.offset]
 
 
 def test_python_binding_raises_on_error(lib):
@@ -149,3 +149,17 @@ def test_q_len_validation(lib):
     call = lambda step: lib.shadowkv_decode_step(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(layer), 16, 16, 16,
                                                  step, 16, None, None, 256, None)
     assert call(1) == bd.SKV_EINVAL and "q_len" in lib.shadowkv_last_error().decode()   # 16 + 1 + 4 > 20
+
+
+def test_ragged_lengths_validation(lib):
+    """Ragged batch (NEXT-3): host and device length arrays together; every s_b in [w + c(o + k), ctx_len]."""
+    import torch
+    mk = lambda t, dev: bd.dims_struct(2, 32, 8, 128, 4096, 160, 8, 4, 8, 16, 40, 1, t, dev)
+    lens = torch.tensor([4096, 3000], dtype=torch.int32)
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(mk(lens, 64))) > 0
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(mk(lens, None))) == 0
+    for bad in ([4097, 3000], [4096, 16 + 8 * 12 - 1]):
+        assert lib.shadowkv_workspace_bytes(ctypes.byref(mk(torch.tensor(bad, dtype=torch.int32), 64))) == 0
+        assert "ctx_lens[" in lib.shadowkv_last_error().decode()
+    shortest = torch.tensor([4096, 16 + 8 * 12], dtype=torch.int32)
+    assert lib.shadowkv_workspace_bytes(ctypes.byref(mk(shortest, 64))) > 0

@@ -1,0 +1,80 @@
+"""Ragged batches (per-request context lengths) through the C ABI vs the oracle.
+
+Every request b of a batch padded to ctx_len has its own length s_b: its own chunk grid, outliers,
+window tail (R8 per request) and decode positions.  The oracle runs each request alone on its own
+s_b tokens (slices of the same seeded inputs); the GPU runs the whole padded batch in one call.
+Build: landmarks within 1 bf16 ulp (R13), outlier sets valid under the min-cos tie rule (R12),
+window tail keys within 1 ulp and values bit-exact.  Decode: the usual selection / key / output
+tolerances (R1, R23) per request, over two steps, from identical state bytes.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import shadowkv_oracle as O
+from tests.parity import assert_bf16_close, check_decode, f64, outliers_valid
+
+pytestmark = pytest.mark.gpu
+
+C1 = synth.CONFIGS["c1"]
+CASES = {
+    "llama_b3": (C1.replace(batch=3, ctx_len=4096, budget=8), [4096, 3001, 2053], [0, 1, 2]),
+    "glm_g16_b2": (C1.replace(batch=2, n_q_heads=32, n_kv_heads=2, rope="glm", ctx_len=2048, budget=12),
+                   [1500, 2048], [0, 1]),
+    "b32_sub_batch_chains": (C1.replace(batch=32, n_q_heads=8, n_kv_heads=2, ctx_len=1024, budget=8, n_outlier=2),
+                             [1024 - 20 * i for i in range(32)], [0, 13, 31]),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_ragged_batch_parity(name):
+    from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
+    cfg, lens, sample = CASES[name]
+    steps, seed = 2, 11
+    c, o, w, k = cfg.chunk, cfg.n_outlier, cfg.window_ctx, cfg.budget
+    inp = synth.gen_layer(cfg, seed)
+    inv, rot, il = synth.rope_table(cfg)
+    shape = Shape.from_config(cfg, steps=steps, ctx_lens=lens)
+    st = LayerState(shape)
+    st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
+    rope = RopeTable(inv, rot, il)
+    ws = alloc_workspace(shape)
+    st.build(rope.struct, ws)
+    torch.cuda.synchronize()
+    A64, B64, V64 = f64(inp["A"]), f64(inp["B"]), f64(inp["V"])
+    ost = {}
+    gids = st.outlier_ids.cpu().numpy()
+    bf = torch.bfloat16
+    for b in sample:
+        sb = lens[b]
+        ob = O.build(A64[b:b + 1, :sb], B64[b:b + 1], V64[b:b + 1, :, :sb], inv, rot, il, c, o, w, shape.window_cap)
+        n_c, w_eff = ob.n_c, ob.w_eff
+        assert_bf16_close(f64(st.landmarks[b, :, :n_c]), ob.landmarks[0], what=f"landmarks b={b}")
+        for h in range(cfg.n_kv_heads):
+            assert outliers_valid(gids[b, h], ob.mincos[0, h], o), f"outliers b={b} h={h}"
+        assert_bf16_close(f64(st.K_win[b, :, :w_eff]), ob.K_win[0, :, :w_eff], what=f"window keys b={b}")
+        assert np.array_equal(f64(st.V_win[b, :, :w_eff]), ob.V_win[0, :, :w_eff]), f"window values b={b}"
+        ost[b] = ob
+        # identical state bytes for decode parity (R13): the oracle's build output for this request
+        st.landmarks[b, :, :n_c].copy_(torch.from_numpy(ob.landmarks[0]).to(bf))
+        st.outlier_ids[b].copy_(torch.from_numpy(ob.outlier_ids[0]).to(torch.int32))
+        st.K_out[b].copy_(torch.from_numpy(ob.K_out[0]).to(bf)); st.V_out[b].copy_(torch.from_numpy(ob.V_out[0]).to(bf))
+        st.K_win[b].copy_(torch.from_numpy(ob.K_win[0]).to(bf)); st.V_win[b].copy_(torch.from_numpy(ob.V_win[0]).to(bf))
+    one = cfg.replace(batch=1)
+    for step in range(steps):
+        si = synth.gen_step(cfg, seed, 0, step)
+        out = torch.empty(cfg.batch, cfg.n_q_heads, cfg.head_dim, dtype=bf, device="cuda")
+        sel = torch.empty(cfg.batch, cfg.n_kv_heads, k, dtype=torch.int32, device="cuda")
+        dbg = torch.empty(cfg.batch, cfg.n_kv_heads, k * c, cfg.head_dim, dtype=bf, device="cuda")
+        st.decode(rope.struct, si["q"].cuda(), si["k_new"].cuda(), si["v_new"].cuda(), step, out, ws,
+                  sel_ids=sel, dbg_keys=dbg)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+        for b in sample:
+            sb = lens[b]
+            oo, os_, oz, ok, ost[b] = O.decode_step(ost[b], A64[b:b + 1, :sb], B64[b:b + 1], V64[b:b + 1, :, :sb],
+                                                    f64(si["q"][b:b + 1]), f64(si["k_new"][b:b + 1]),
+                                                    f64(si["v_new"][b:b + 1]), step, k, inv, rot, il, c)
+            assert sel[b].max().item() < ost[b].n_c, "selected a chunk past the request's own grid"
+            check_decode(one, f64(out[b:b + 1]), sel[b:b + 1].cpu().numpy(), f64(dbg[b:b + 1]), oo, os_, oz, ok)
