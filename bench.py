@@ -347,6 +347,8 @@ def multi_query_leg(args, cfg, q_len, states, rope, seed, host_bytes, host_peak,
     per step (all accepted: an upper bound for speculative decoding, the attention cost per call)."""
     from paper_2410_21465_b200 import LayerState, Shape, alloc_workspace, shard
     import copy
+    if (cfg.n_q_heads // cfg.n_kv_heads) * q_len > 16:
+        return {"skipped": f"GQA group x s_q = {(cfg.n_q_heads // cfg.n_kv_heads) * q_len} > 16 rows", "q_len": q_len}
     Lm, b = cfg.n_layers, cfg.batch
     n_states = len(states)
     steps, warm = args.steps, max(args.warmup, 3)

@@ -248,6 +248,30 @@ __device__ __forceinline__ int block_sum(int x, int* wsum) {
   return t;
 }
 
+// z_j over the G rows of a KV head = (q head, query token) pairs, SQ tokens per q head (rows hq*SQ + i):
+// z = max_hq log sum_i exp(l_{hq,i} - lse_{hq,i})  (softmax, sum over s_q, group max; R4, R5);
+// SQ = 1 is the plain max of (l - lse).
+template <int G, int SQ>
+__device__ __forceinline__ float group_z(const float* lg, const float* lse) {
+  float zz = -INFINITY;
+  if constexpr (SQ == 1 || G % SQ != 0) {
+#pragma unroll
+    for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lg[hq] - lse[hq]);
+  } else {
+#pragma unroll
+    for (int r0 = 0; r0 < G; r0 += SQ) {
+      float m = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < SQ; ++i) m = fmaxf(m, lg[r0 + i] - lse[r0 + i]);
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < SQ; ++i) acc += expf(lg[r0 + i] - lse[r0 + i] - m);
+      zz = fmaxf(zz, m > -INFINITY ? m + logf(acc) : -INFINITY);
+    }
+  }
+  return zz;
+}
+
 template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 2)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
@@ -322,20 +346,13 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT + tid;
-      float zz = -INFINITY;
-      if (sq == 1) {
-#pragma unroll
-        for (int hq = 0; hq < G; ++hq) zz = fmaxf(zz, lg[u][hq] - lse[hq]);
-      } else {             // s_q query tokens per q head (rows hq*s_q + i): z = max_hq log sum_i S_{hq,i}
-        for (int r0 = 0; r0 < G; r0 += sq) {
-          float m = -INFINITY;
-          for (int i = 0; i < sq; ++i) m = fmaxf(m, lg[u][r0 + i] - lse[r0 + i]);
-          if (m > -INFINITY) {
-            float acc = 0.f;
-            for (int i = 0; i < sq; ++i) acc += expf(lg[u][r0 + i] - lse[r0 + i] - m);
-            zz = fmaxf(zz, m + logf(acc));
-          }
-        }
+      float zz;
+      switch (sq) {        // compile-time s_q: the row array stays in registers
+        case 1: zz = group_z<G, 1>(lg[u], lse); break;
+        case 2: zz = group_z<G, 2>(lg[u], lse); break;
+        case 4: zz = group_z<G, 4>(lg[u], lse); break;
+        case 8: zz = group_z<G, 8>(lg[u], lse); break;
+        default: zz = group_z<G, 16>(lg[u], lse); break;
       }
       if (j < len) {
         z[j] = zz;

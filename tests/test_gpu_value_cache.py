@@ -22,6 +22,7 @@ CASES = {
     "c1_k16": C1.replace(ctx_len=2048, budget=16),
     "g16_multi_unit": C1.replace(n_q_heads=32, n_kv_heads=2, rope="glm", ctx_len=8192, budget=40, n_outlier=6),
     "g1_batch2_ragged": C1.replace(batch=2, n_q_heads=8, n_kv_heads=8, ctx_len=3001, budget=12),
+    "b32_sub_batch_chains": C1.replace(batch=32, n_q_heads=8, n_kv_heads=2, ctx_len=1024, budget=8, n_outlier=2),
 }
 
 

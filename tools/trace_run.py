@@ -19,10 +19,11 @@ ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--raw-epi", action="store_true", help="score events 8-11 hold clock64 deltas")
 ap.add_argument("--slots", type=int, default=1, help="trace this many consecutive layers (steady state)")
 ap.add_argument("--vc-rho", type=float, default=None, help="value cache on, queries drifting with this rho")
+ap.add_argument("--q-len", type=int, default=1, help="s_q query tokens per call")
 args = ap.parse_args()
 os.environ["SKV_TRACE_SLOTS"] = str(args.slots)
 cfg = synth.CONFIGS[args.config]
-shape = Shape.from_config(cfg, steps=64)
+shape = Shape.from_config(cfg, steps=64, q_len=args.q_len)
 inv, rot, il = synth.rope_table(cfg)
 rope = RopeTable(inv, rot, il)
 ws = alloc_workspace(shape)
@@ -33,11 +34,16 @@ for l in range(args.layers):
     st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
     st.build(rope.struct, ws)
     states.append(st)
-out = torch.empty(cfg.batch, cfg.n_q_heads, 128, dtype=torch.bfloat16, device="cuda")
+out = torch.empty(cfg.batch, cfg.n_q_heads, args.q_len, 128, dtype=torch.bfloat16, device="cuda")
 SLOT = 4 * 4096 * 16
 tr = torch.zeros(args.slots * SLOT, dtype=torch.int64, device="cuda")
 first = args.layers - args.slots
 sis = [[synth.gen_step(cfg, 99, l, step, device="cuda") for l in range(args.layers)] for step in range(6)]
+if args.q_len > 1:
+    for step in range(6):
+        for l in range(args.layers):
+            si = sis[step][l]
+            sis[step][l] = {n: si[n].unsqueeze(2).repeat(1, 1, args.q_len, 1).contiguous() for n in si}
 if args.vc_rho is not None:
     for l in range(args.layers):
         qd = synth.gen_q_drift(cfg, 99, l, 6, args.vc_rho, device="cuda")
@@ -50,7 +56,7 @@ for step in range(6):
             torch.cuda.synchronize()
             tr.zero_()
             bd.shadowkv_trace_buffer(tr)
-        st.decode(rope.struct, si["q"], si["k_new"], si["v_new"], step, out, ws)
+        st.decode(rope.struct, si["q"], si["k_new"], si["v_new"], step * args.q_len, out, ws)
     if step == 5:
         torch.cuda.synchronize()
         bd.shadowkv_trace_buffer(None)
