@@ -435,7 +435,7 @@ def run_ours(args, cfg):
     dev_layer = 2 * b * (cfg.ctx_len * cfg.rank + cfg.n_kv_heads * (shape.n_c * cfg.head_dim + cfg.rank * cfg.head_dim
                                                                      + 2 * (cfg.n_outlier * cfg.chunk + shape.window_cap) * cfg.head_dim))
     import psutil
-    host_cap = int(0.35 * psutil.virtual_memory().available / world // (per_layer * 2))   # page-locking more failed (c5)
+    host_cap = int(0.6 * psutil.virtual_memory().available / world // (per_layer * 2))   # c5: pass --layer-states 8
     dev_cap = int(0.7 * torch.cuda.mem_get_info()[0] // dev_layer)
     n_states = args.layer_states or max(1, min(Lm, host_cap, dev_cap))
     if per_layer * 2 * n_states > 0.8 * psutil.virtual_memory().available / world:
