@@ -590,6 +590,19 @@ def run_ours(args, cfg):
                 "peak_note": "pinned H2D copy-engine bandwidth measured live in this run (1 GiB, best of 6); "
                              "zero-copy SM loads saturate ~51 GB/s (profiles/r01_probe_hostlink.txt)"}
 
+    # --- selection adjacency: mean run length of consecutive selected chunk ids, so that
+    #     contiguity is not silently helping the host link (2 KB pieces are fetched independently anyway)
+    sel_ids = torch.empty(b, cfg.n_kv_heads, cfg.budget, dtype=torch.int32, device=dev)
+    runs = []
+    for l in range(min(4, n_states)):
+        q0, k0, v0 = dev_inputs[l % len(dev_inputs)]
+        states[l].decode(rope.struct, q0[l], k0[l], v0[l], n_total - 1, out[l], ws, sel_ids=sel_ids, stream=stream)
+        ids = sel_ids.cpu().numpy().reshape(-1, cfg.budget)
+        for row in ids:
+            runs.append(cfg.budget / (1 + int(((row[1:] - row[:-1]) != 1).sum())))
+    selection = {"mean_run_length_chunks": float(sum(runs) / len(runs)), "chunks_per_kv_head": cfg.budget,
+                 "sample": f"{len(runs)} (layer, request, KV head) selections at the last step index"}
+
     value_cache = None
     if args.vc_rho:
         value_cache = [value_cache_leg(args, cfg, float(r), states, rope, ws, out, stream, seed, host_bytes, host_peak,
@@ -618,6 +631,7 @@ def run_ours(args, cfg):
                            launch="one CUDA graph per 32-layer step (shadowkv_decode_step_dev)" if use_graph
                            else "stream launches (shadowkv_decode_step)"),
             "roofline": roofline,
+            "selection": selection,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": gpu_launches,

@@ -193,10 +193,10 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
       }
     }
     __syncthreads();                                   // Pb complete; stage `st` free for reuse
-    float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c + j0;
+    float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * D.n_c + (size_t)j0 * G;   // [n_c][G]
     for (int idx = tid; idx < G * kSTile; idx += 256) {
-      const int hq = idx / kSTile, r = idx - hq * kSTile;
-      if (r < rows) lb[(size_t)hq * D.n_c + r] = Pb[idx];
+      const int r = idx / G, hq = idx - r * G;
+      if (r < rows) lb[idx] = Pb[hq * kSTile + r];
     }
     for (int hq = warp; hq < G; hq += 8) {           // tile softmax partial merged into the segment's
       float x[kSTile / 32];
@@ -298,7 +298,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   const int n_per = (n + kSelCL - 1) / kSelCL;
   const int lo = min(n, (int)crank * n_per), len = min(n, lo + n_per) - lo;
   float* z = ZSMEM ? zdyn : zws + bh * n + lo;           // this CTA's z slice
-  const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * n + lo;
+  const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * n + (size_t)lo * G;   // [n][G]
   int32_t* out = sel + bh * k;
   trace(1, 0);
   if (early_trigger) pdl_trigger();                     // sparse-attn CTAs may start their prologue
@@ -341,7 +341,8 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT + tid;
 #pragma unroll
-      for (int hq = 0; hq < G; ++hq) lg[u][hq] = j < len ? lb[(size_t)hq * n + j] : -INFINITY;
+      for (int hq = 0; hq < G; ++hq) lg[u][hq] = -INFINITY;
+      if (j < len) load_row<G>(lb + (size_t)j * G, lg[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {

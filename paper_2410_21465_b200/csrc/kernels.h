@@ -53,7 +53,8 @@ struct DecodeWs {
   int* counters;     // [b][hk] zero-initialised by the caller once; every call leaves them zero
   int* flags;        // [b][hk][4] {score_done, slots_reserved, -, -}; zeroed again by each call's merger
   int32_t* selrest;  // [b][hk][k] radix-fallback scratch (top-k, ascending)
-  float* logits;     // [b][hq][n_c]
+  float* logits;     // [b][hk][n_c][G]: landmark-major, the G rows of a landmark contiguous (one vector
+                     // store in the score epilogue, one vector load per landmark in k_select)
   float2* part;      // [b][hq][kSegMax] per-(score CTA, head) softmax partials (max, sumexp)
   float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
   int32_t* sel;      // [b][hk][k] published selection, unordered, chunk id + 1 (0 = not yet); re-zeroed

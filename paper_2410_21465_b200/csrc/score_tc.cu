@@ -307,10 +307,13 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       const bool out = ((obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u) || j >= ncb;
       if (warp == 0 && lane == 0 && i < 4) trace_tc_any(trace_buf, 8 + i);   // epilogue got tile i
       if (j < D.n_c) {
+        float xs[G];
+#pragma unroll
+        for (int hq = 0; hq < G; ++hq) xs[hq] = out ? -INFINITY : v[hq] * scale;
+        store_row<G>(lrow + (size_t)j * G, xs);             // landmark-major logits [n_c][G]
 #pragma unroll
         for (int hq = 0; hq < G; ++hq) {
-          const float x = out ? -INFINITY : v[hq] * scale;
-          lrow[(size_t)hq * D.n_c + j] = x;
+          const float x = xs[hq];
           const float x2 = out ? kFloor : x * kLog2e;
           const float mn = fmaxf(m_run[hq], x2);
           s_run[hq] = fmaf(s_run[hq], exp2f(m_run[hq] - mn), out ? 0.f : exp2f(x2 - mn));
