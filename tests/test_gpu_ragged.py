@@ -27,16 +27,19 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("name", list(CASES))
-def test_ragged_batch_parity(name):
+@pytest.mark.parametrize("name,q_len,value_cache", [(n, 1, False) for n in CASES] +
+                         [("llama_b3", 2, True), ("b32_sub_batch_chains", 4, True)])
+def test_ragged_batch_parity(name, q_len, value_cache):
+    """(+ s_q > 1 query tokens and the value cache on the same ragged batch: every NEXT-3 / NEXT-1
+    feature at once; with the cache, results are also bit-identical to a cache-less twin)."""
     from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
     cfg, lens, sample = CASES[name]
-    steps, seed = 2, 11
+    steps, seed = (3 if value_cache else 2), 11
     c, o, w, k = cfg.chunk, cfg.n_outlier, cfg.window_ctx, cfg.budget
     inp = synth.gen_layer(cfg, seed)
     inv, rot, il = synth.rope_table(cfg)
-    shape = Shape.from_config(cfg, steps=steps, ctx_lens=lens)
-    st = LayerState(shape)
+    shape = Shape.from_config(cfg, steps=steps, ctx_lens=lens, q_len=q_len)
+    st = LayerState(shape, value_cache=value_cache)
     st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
     rope = RopeTable(inv, rot, il)
     ws = alloc_workspace(shape)
@@ -61,16 +64,36 @@ def test_ragged_batch_parity(name):
         st.outlier_ids[b].copy_(torch.from_numpy(ob.outlier_ids[0]).to(torch.int32))
         st.K_out[b].copy_(torch.from_numpy(ob.K_out[0]).to(bf)); st.V_out[b].copy_(torch.from_numpy(ob.V_out[0]).to(bf))
         st.K_win[b].copy_(torch.from_numpy(ob.K_win[0]).to(bf)); st.V_win[b].copy_(torch.from_numpy(ob.V_win[0]).to(bf))
+    twin = None
+    if value_cache:
+        twin = LayerState(shape, V_host=st.V_host)
+        for n in ("A", "B", "landmarks", "outlier_ids", "K_out", "V_out", "K_win", "V_win"):
+            getattr(twin, n).copy_(getattr(st, n))
     one = cfg.replace(batch=1)
-    for step in range(steps):
-        si = synth.gen_step(cfg, seed, 0, step)
-        out = torch.empty(cfg.batch, cfg.n_q_heads, cfg.head_dim, dtype=bf, device="cuda")
+    qd = synth.gen_q_drift(cfg, seed, 0, steps * q_len, 0.97)           # drifting: the cache gets hits
+    for call in range(steps):
+        step = call * q_len
+        toks = [synth.gen_step(cfg, seed, 0, step + i) for i in range(q_len)]
+        for i, t in enumerate(toks):
+            t["q"] = qd[step + i]
+        if q_len == 1:
+            si = toks[0]
+        else:
+            si = {n: torch.stack([t[n] for t in toks], dim=2) for n in ("q", "k_new", "v_new")}
+        out = torch.empty(si["q"].shape, dtype=bf, device="cuda")
         sel = torch.empty(cfg.batch, cfg.n_kv_heads, k, dtype=torch.int32, device="cuda")
         dbg = torch.empty(cfg.batch, cfg.n_kv_heads, k * c, cfg.head_dim, dtype=bf, device="cuda")
         st.decode(rope.struct, si["q"].cuda(), si["k_new"].cuda(), si["v_new"].cuda(), step, out, ws,
                   sel_ids=sel, dbg_keys=dbg)
         torch.cuda.synchronize()
         assert torch.isfinite(out.float()).all()
+        if twin is not None:
+            out2 = torch.empty_like(out)
+            sel2 = torch.empty_like(sel)
+            twin.decode(rope.struct, si["q"].cuda(), si["k_new"].cuda(), si["v_new"].cuda(), step, out2, ws,
+                        sel_ids=sel2)
+            torch.cuda.synchronize()
+            assert torch.equal(out, out2) and torch.equal(sel, sel2), "value cache changed a ragged result"
         for b in sample:
             sb = lens[b]
             oo, os_, oz, ok, ost[b] = O.decode_step(ost[b], A64[b:b + 1, :sb], B64[b:b + 1], V64[b:b + 1, :, :sb],
@@ -78,3 +101,5 @@ def test_ragged_batch_parity(name):
                                                     f64(si["v_new"][b:b + 1]), step, k, inv, rot, il, c)
             assert sel[b].max().item() < ost[b].n_c, "selected a chunk past the request's own grid"
             check_decode(one, f64(out[b:b + 1]), sel[b:b + 1].cpu().numpy(), f64(dbg[b:b + 1]), oo, os_, oz, ok)
+    if value_cache:
+        assert int(st.cache_stats()[..., 3].sum()) > 0, "drifting queries produced no cache hits"
