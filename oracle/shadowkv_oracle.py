@@ -26,7 +26,7 @@ __all__ = [
     "bf16_round", "identity_store", "partition", "rope", "chunk_means", "chunk_min_cos",
     "smallest_o", "build", "BuildState", "landmark_scores", "normalise_group_max",
     "arg_topk", "rebuild_keys", "decode_step", "dense_attention", "softmax_attention",
-    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits", "factorize", "normalise_sum_group_max",
+    "equivalent_bandwidth", "jacobi_svd", "ValueChunkCache", "replay_hits", "factorize", "normalise_sum_group_max", "lowrank_generated_keys",
 ]
 
 
@@ -328,6 +328,24 @@ def _decode_step_multi(state, A, B, V, q, k_new, v_new, step, k, inv_freq, rotar
                 for j in range(g):
                     out[bi, h * g + j, i] = softmax_attention(qg[j, i], keys[order], vals[order])
     return out, sel, Z, Kt, st
+
+
+def lowrank_generated_keys(k_pre, B, positions, inv_freq, rotary_dim, interleaved, store=bf16_round):
+    """Low-rank storage of generated keys (P:196 footnote): "new pre-RoPE keys K' can be
+    stored as K' Psi and projected back with Psi^T when needed", Psi = the right singular matrix of the
+    context's pre-RoPE keys.  With the heads concatenated (R14) Psi[(h, j), rho] = B_h[rho, j], so the
+    stored state of a generated token is one rank-r row a = sum_h k'_h B_h^T (like a row of A), kept
+    at storage precision, and the key attended is RoPE_t(a B_h) at the token's position t.
+    k_pre [b][h_kv][n][d] (n generated tokens), B [b][h_kv][r][d], positions [n].
+    Returns (a [b][n][r] as stored, keys [b][h_kv][n][d] post-RoPE, unrounded)."""
+    k_pre = np.asarray(k_pre, np.float64); B = np.asarray(B, np.float64)
+    nb, hk, n, d = k_pre.shape
+    a = store(np.einsum("bhnd,bhrd->bnr", k_pre, B))
+    keys = np.zeros((nb, hk, n, d))
+    for bi in range(nb):
+        for h in range(hk):
+            keys[bi, h] = rope(a[bi] @ B[bi, h], np.asarray(positions), inv_freq, rotary_dim, interleaved)
+    return a, keys
 
 
 # ----------------------------------------------------------------------------

@@ -68,3 +68,41 @@ def test_factor_structure():
     np.testing.assert_allclose(A[0].T @ A[0], np.diag(sig[0, :r] ** 2), atol=1e-9)
     G = sum(B[0, h] @ B[0, h].T for h in range(2))
     np.testing.assert_allclose(G, np.eye(r), atol=1e-12)
+
+
+# ---------------------------------------------------------------- NEXT-4: low-rank generated keys
+def _inv(d):
+    return (1.0 / 10000 ** (np.arange(0, d, 2) / d)).astype(np.float32)
+
+
+def test_lowrank_generated_key_exact_inside_the_subspace():
+    """A generated pre-RoPE key that lies in the context's rank-r subspace is reproduced exactly:
+    Psi Psi^T k' = k' (orthonormal Psi from the SVD), so the attended key is RoPE_t(k')."""
+    rng = np.random.default_rng(30)
+    K = _keys(rng, 1, 2, 64, 8, 6)
+    A, B, _ = O.factorize(K, 6)
+    Vt = B[0].transpose(1, 0, 2).reshape(6, 16)                          # Psi^T, heads concatenated
+    kp = (rng.normal(size=(1, 6)) @ Vt).reshape(1, 2, 1, 8)              # [b][h][n=1][d], inside the span
+    pos = np.array([70])
+    a, keys = O.lowrank_generated_keys(kp, B, pos, _inv(8), 8, False, store=O.identity_store)
+    want = np.stack([O.rope(kp[0, h], pos, _inv(8), 8, False) for h in range(2)])
+    np.testing.assert_allclose(keys[0], want, atol=1e-12)
+
+
+def test_lowrank_generated_key_error_is_the_distance_to_the_subspace():
+    """Pythagoras with orthonormal Psi: ||k'||^2 = ||a||^2 + ||k' - a Psi^T||^2 (pre-RoPE; RoPE is an
+    isometry, so the post-RoPE error is the same), and a is r numbers instead of h_kv * d."""
+    rng = np.random.default_rng(31)
+    K = _keys(rng, 1, 3, 80, 8, 24, noise=0.1)
+    r = 8
+    A, B, _ = O.factorize(K, r)
+    kp = rng.normal(size=(1, 3, 2, 8))
+    pos = np.array([90, 91])
+    a, keys = O.lowrank_generated_keys(kp, B, pos, _inv(8), 8, False, store=O.identity_store)
+    assert a.shape == (1, 2, r)
+    for n in range(2):
+        x = kp[0, :, n].reshape(-1)
+        rec = np.concatenate([a[0, n] @ B[0, h] for h in range(3)])
+        assert abs(x @ x - (a[0, n] @ a[0, n] + (x - rec) @ (x - rec))) < 1e-10
+        exact = np.stack([O.rope(kp[0, h, n:n + 1], pos[n:n + 1], _inv(8), 8, False)[0] for h in range(3)])
+        assert abs(np.linalg.norm(keys[0, :, n] - exact) - np.linalg.norm(x - rec)) < 1e-10
