@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--q-len-leg", type=int, default=4,
                     help="multi-query leg (NEXT-3, Alg 2's s_q): the same 32-layer step with s_q query tokens per "
                          "call (speculative verification); 0 = skip")
+    ap.add_argument("--lowrank-gen-leg", type=int, default=1,
+                    help="low-rank generated keys leg (NEXT-4, P:196): the same step with skv_layer.A_gen; 0 = skip")
     ap.add_argument("--layer-states", type=int, default=0,
                     help="distinct layer states cycled per step (default: the model's layer count)")
     return ap.parse_args()
@@ -406,6 +408,61 @@ def multi_query_leg(args, cfg, q_len, states, rope, seed, host_bytes, host_peak,
 
 
 # ------------------------------------------------------------------------------------------------
+def lowrank_gen_leg(args, cfg, states, rope, ws, seed, dev):
+    """NEXT-4 (P:196 footnote): the same graph-timed 32-layer step with skv_layer.A_gen, i.e. every
+    generated token's key stored as one rank-r row (pre-RoPE k_new projected on the B rows) and rebuilt
+    when attended, instead of h_kv*d post-RoPE values in the window."""
+    import copy
+    from paper_2410_21465_b200 import shard
+    Lm, b = cfg.n_layers, cfg.batch
+    n_states = len(states)
+    steps, warm = args.steps, max(args.warmup, 3)
+    try:
+        layers = []
+        for l in range(n_states):
+            st = copy.copy(states[l])
+            st.A_gen = torch.zeros(b, st.shape.window_cap, cfg.rank, dtype=torch.bfloat16, device=dev)
+            layers.append(st)
+    except torch.OutOfMemoryError:
+        return {"skipped": "out of HBM"}
+    gen = torch.Generator(device=dev).manual_seed(seed + 4242)
+    q_g = (2.0 * torch.randn(Lm, b, cfg.n_q_heads, cfg.head_dim, device=dev, generator=gen)).to(torch.bfloat16)
+    k_g = torch.randn(Lm, b, cfg.n_kv_heads, cfg.head_dim, device=dev, generator=gen).to(torch.bfloat16)
+    v_g = torch.randn(Lm, b, cfg.n_kv_heads, cfg.head_dim, device=dev, generator=gen).to(torch.bfloat16)
+    qs = [(2.0 * torch.randn(q_g.shape, device=dev, generator=gen)).to(torch.bfloat16) for _ in range(4)]
+    out = torch.empty(Lm, b, cfg.n_q_heads, cfg.head_dim, dtype=torch.bfloat16, device=dev)
+    step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+    max_step = steps + warm
+    cap = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        for l in range(Lm):
+            layers[l % n_states].decode_dev(rope.struct, q_g[l], k_g[l], v_g[l], step_dev, max_step, out[l], ws, stream=cap)
+        step_dev.add_(1)
+    step_dev.fill_(0)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    for i in range(warm):
+        q_g.copy_(qs[i % 4], non_blocking=True)
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        q_g.copy_(qs[i % 4], non_blocking=True)
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    value = shard.job_tokens_per_s(b, ms / 1e3, device=dev)
+    del g, layers
+    torch.cuda.empty_cache()
+    return {"value": value, "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
+            "key_bytes_per_generated_token": cfg.rank * 2, "plain_window_key_bytes": cfg.n_kv_heads * cfg.head_dim * 2,
+            "note": "generated keys stored as rank-r rows (K' Psi, P:196) and rebuilt with RoPE when attended"}
+
+
+# ------------------------------------------------------------------------------------------------
 def run_ours(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -612,6 +669,10 @@ def run_ours(args, cfg):
     if args.q_len_leg and args.q_len_leg > 1:
         multi_query = multi_query_leg(args, cfg, args.q_len_leg, states, rope, seed, host_bytes, host_peak, dev)
 
+    lowrank_gen = None
+    if args.lowrank_gen_leg:
+        lowrank_gen = lowrank_gen_leg(args, cfg, states, rope, ws, seed, dev)
+
     breakdown = None
     if args.breakdown:
         bd.shadowkv_profile_begin(Lm * 5 * 20 + 8, 0x1F)
@@ -642,6 +703,8 @@ def run_ours(args, cfg):
         line["value_cache"] = value_cache[0] if len(value_cache) == 1 else value_cache
     if multi_query:
         line["multi_query"] = multi_query
+    if lowrank_gen:
+        line["lowrank_gen"] = lowrank_gen
     if breakdown:
         line["kernel_breakdown_us"] = breakdown
     if world == 1 and not args.no_cpu_baseline:

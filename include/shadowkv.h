@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SHADOWKV_ABI_VERSION 4
+#define SHADOWKV_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define SKV_API __attribute__((visibility("default")))
@@ -121,6 +121,14 @@ typedef struct {
                                the step that last wrote the chunk; zero = never cached          */
   uint64_t *vc_stats;       /* device [b][h_kv][4]: {generation (decode steps run), scratch,
                                hits in the last step, hits in total}; read them after a sync    */
+  /* Optional low-rank storage of generated keys (P:196 footnote "new pre-RoPE keys K' can be stored
+   * as K' Psi and projected back with Psi^T").  NULL = plain window.  Non-NULL: decode's
+   * k_new is PRE-RoPE; each generated token g (= step + i) is stored as one rank-r row
+   * A_gen[b][g][:] = bf16(sum_h k'_h B_h^T) (Psi[(h, j), rho] = B_h[rho][j], R14) -- r values per token
+   * for all heads instead of h_kv*d -- and attended with the key RoPE_{s_b+g}(A_gen[b][g] . B_h);
+   * K_win slots >= w_eff are then neither written nor read (values still go to V_win).  Exact when
+   * k' lies in the span of the B rows (e.g. B from shadowkv_factorize). */
+  uint16_t *A_gen;          /* device bf16 [b][window_cap][r]                                    */
 } skv_layer;
 
 /* Bytes of scratch `workspace` (device, 256-byte aligned) that build_cache and decode_step need
@@ -155,7 +163,7 @@ SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *ro
  *   a6  out_hq = softmax attention of q_hq over outlier tokens + K~/V~ + window slots
  *       [0, w_eff+step] (R17)
  * q      device bf16 [b][h_q][s_q][d], token i post-RoPE at position s+step+i (R16)
- * k_new  device bf16 [b][h_kv][s_q][d] post-RoPE;  v_new device bf16 [b][h_kv][s_q][d]
+ * k_new  device bf16 [b][h_kv][s_q][d] post-RoPE (pre-RoPE with layer.A_gen);  v_new [b][h_kv][s_q][d]
  *        (written to window slots w_eff+step .. w_eff+step+s_q-1; the next call's step is step+s_q)
  * out    device bf16 [b][h_q][s_q][d]
  * sel_ids   nullable device int32 [b][h_kv][k]  -- parity hook for a3

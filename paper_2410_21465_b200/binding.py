@@ -37,7 +37,7 @@ class SkvRope(ctypes.Structure):
 class SkvLayer(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("A", "B", "landmarks", "outlier_ids", "K_out", "V_out", "K_win", "V_win", "V_host",
-                 "vc_values", "vc_dir", "vc_stats")]
+                 "vc_values", "vc_dir", "vc_stats", "A_gen")]
 
 
 class ShadowKVError(RuntimeError):
@@ -122,9 +122,10 @@ def rope_struct(rotary_dim: int, interleaved: bool, inv_freq) -> SkvRope:
 
 
 def layer_struct(A, B, landmarks, outlier_ids, K_out, V_out, K_win, V_win, V_host,
-                 vc_values=None, vc_dir=None, vc_stats=None) -> SkvLayer:
+                 vc_values=None, vc_dir=None, vc_stats=None, A_gen=None) -> SkvLayer:
     return SkvLayer(_ptr(A), _ptr(B), _ptr(landmarks), _ptr(outlier_ids), _ptr(K_out), _ptr(V_out),
-                    _ptr(K_win), _ptr(V_win), _ptr(V_host), _ptr(vc_values), _ptr(vc_dir), _ptr(vc_stats))
+                    _ptr(K_win), _ptr(V_win), _ptr(V_host), _ptr(vc_values), _ptr(vc_dir), _ptr(vc_stats),
+                    _ptr(A_gen))
 
 
 def shadowkv_workspace_bytes(dims: SkvDims) -> int:

@@ -103,8 +103,9 @@ skv_status check_layer(const skv_layer* l, const skv::Dims& D, skv::Layer* Ly) {
   if (n_vc != 0 && n_vc != 3) return fail(SKV_EINVAL, "layer.vc_values / vc_dir / vc_stats: give all three or none");
   if (n_vc && (!aligned16(l->vc_values) || !aligned16(l->vc_dir) || !aligned16(l->vc_stats)))
     return fail(SKV_EINVAL, "layer.vc_* must be 16-byte aligned");
+  if (l->A_gen && (reinterpret_cast<uintptr_t>(l->A_gen) & 15u)) return fail(SKV_EINVAL, "layer.A_gen must be 16-byte aligned");
   *Ly = skv::Layer{l->A, l->B, l->landmarks, l->outlier_ids, l->K_out, l->V_out, l->K_win, l->V_win, l->V_host,
-                   l->vc_values, reinterpret_cast<unsigned long long*>(l->vc_dir),
+                   l->A_gen, l->vc_values, reinterpret_cast<unsigned long long*>(l->vc_dir),
                    reinterpret_cast<unsigned long long*>(l->vc_stats)};
   return SKV_OK;
 }
@@ -298,6 +299,8 @@ static skv_status decode_impl(const skv_dims* dims, const skv_rope* rope, const 
   if ((st = check_rope(rope, D.d, &R)) != SKV_OK) return st;
   if ((st = check_layer(layer, D, &Ly)) != SKV_OK) return st;
   if (step < 0) return fail(SKV_EINVAL, "step must be >= 0");
+  D.lr_A = Ly.A_gen;                                     // low-rank generated keys (NEXT-4)
+  D.lr_B = Ly.A_gen ? Ly.B : nullptr;
   if (D.w_eff + step + D.sq > D.wcap)
     return fail(SKV_EINVAL, "window overflow: w_eff %d + step %d + q_len %d > window_cap %d", D.w_eff, step, D.sq,
                 D.wcap);

@@ -20,6 +20,7 @@
 // Kernels after the first are launched with programmatic dependent launch (PDL).
 #include <cstdlib>
 
+#include "append.cuh"
 #include "kernels.h"
 #include "topk.cuh"
 
@@ -127,13 +128,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
   pdl_trigger();                                       // let the select grid become resident early
   // a7: append the current token's K, V to the window (R18)
   const int stp = cur_step(D, step);
-  for (int idx = blockIdx.x * 256 + tid; idx < D.b * D.hk * D.sq * 32; idx += gridDim.x * 256) {
-    const int bhi = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;    // (b, h, new token i)
-    const int bh = bhi / D.sq, i = bhi - bh * D.sq;
-    const size_t dst = ((size_t)bh * D.wcap + req_weff(D, bh / D.hk) + stp + i) * kHeadDim + p * 8;
-    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bhi * kHeadDim + p * 8;
-    *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
-  }
+  window_append(D, k_new, v_new, K_win, V_win, stp, blockIdx.x * 256 + tid, gridDim.x * 256);
   if (tid == 0) {
     for (int st = 0; st < kSStages; ++st) mbar_init(&full[st], 1);
     fence_mbar_init();
@@ -651,7 +646,7 @@ __global__ void __launch_bounds__(256, 2)
 k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t* __restrict__ sel,
               int* __restrict__ flags, int step,
               float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
-              int n_split, float scale, uint16_t* __restrict__ dbg, int early_next) {
+              int n_gen_u, int n_split, float scale, uint16_t* __restrict__ dbg, int early_next) {
   TRACE_INIT;
   extern __shared__ __align__(128) uint8_t smem[];
   const AttnSmem lay = attn_smem_layout(D.r, G);
@@ -669,17 +664,31 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   const int stp0 = cur_step(D, step);
   const int T_out = D.o * kChunk;
   int T_win;                                           // this request's window incl. the s_q new tokens
-  int u = blockIdx.x, kind, bh, ui;
-  if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; }
+  // unit kinds: 0 selected chunks, 1 outliers, 2 window (plain: context tail + generated; low-rank: tail
+  // only), 3 generated tokens rebuilt from their low-rank rows (NEXT-4)
+  const bool lowrank = D.lr_A != nullptr;
+  int u = blockIdx.x, kind, bh, ui, split;
+  if (u < BH * n_sel_u) { kind = 0; bh = u / n_sel_u; ui = u - bh * n_sel_u; split = ui; }
   else {
     u -= BH * n_sel_u;
-    const int per = n_out_u + n_win_u;
+    const int per = n_out_u + n_win_u + n_gen_u;
     bh = u / per; ui = u - bh * per;
-    if (ui < n_out_u) kind = 1; else { kind = 2; ui -= n_out_u; }
+    split = n_sel_u + ui;
+    if (ui < n_out_u) kind = 1;
+    else if (ui < n_out_u + n_win_u) { kind = 2; ui -= n_out_u; }
+    else { kind = 3; ui -= n_out_u + n_win_u; }
   }
   const int b = bh / D.hk, h = bh - b * D.hk;
-  T_win = req_weff(D, b) + stp0 + D.sq;
-  const int split = kind == 0 ? ui : (kind == 1 ? n_sel_u + ui : n_sel_u + n_out_u + ui);
+  T_win = lowrank ? req_weff(D, b) : req_weff(D, b) + stp0 + D.sq;
+  const int n_gen = stp0 + D.sq;                                // generated tokens incl. this call's
+  if (kind == 3 && ui * kUnitTok >= n_gen) {                    // generated unit past the live tokens
+    for (int hq = tid >> 7; hq < G; hq += 2) {
+      const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+      o_part[row * kHeadDim + (tid & 127)] = 0.f;
+      if ((tid & 127) == 0) ml_part[row] = make_float2(-INFINITY, 0.f);
+    }
+    return;
+  }
   int32_t* slots = sel + (size_t)bh * D.k;                     // k_select's unordered selection (id + 1)
   const int nch = kind == 0 ? min(8, D.k - ui * 8) : 0;        // chunks of a selected-chunk unit (>= 1)
   trace(2, 0);
@@ -695,15 +704,27 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   unsigned long long vc_gen = 0;
   const int tx = tid & 15, ty = tid >> 4;      // key-tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
   float acc[4][8];
-  if (kind == 0) {
+  if (kind == 0 || kind == 3) {
     const size_t bbytes = (size_t)D.r * kHeadDim * 2;
     if (tid == 0) {   // B_h does not depend on the selection: fetch it before the PDL wait
       asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&barAB)), "r"((uint32_t)bbytes) : "memory");
       bulk_g2s(Bs, Ly.B + (size_t)bh * D.r * kHeadDim, (uint32_t)bbytes, &barAB);
     }
+    if (kind == 3) {  // generated tokens g0 .. g0+ntok-1: low-rank rows + values, positions s_b + g (R16)
+      const int g0 = ui * kUnitTok, nt = min(kUnitTok, n_gen - g0);
+      cta_wait_flag(&flags[(size_t)bh * 4]);                    // (score's a7 projection is visible)
+      if (tid == 0) {
+        mbar_expect_tx(&barAB, nt * D.r * 2);
+        bulk_g2s(As, D.lr_A + ((size_t)b * D.wcap + g0) * D.r, nt * D.r * 2, &barAB);
+        mbar_expect_tx(&barV, nt * kHeadDim * 2);
+        bulk_g2s(Vs, Ly.V_win + ((size_t)bh * D.wcap + req_weff(D, b) + g0) * kHeadDim, nt * kHeadDim * 2, &barV);
+      }
+      if (tid < kUnitTok) tok[tid] = tid < nt ? req_s(D, b) + g0 + tid : 0;
+    }
     // thread c < nch waits for its slot, then issues its chunk's two copies at once: the value fetch
     // of each chunk starts the moment k_select publishes it
-    if (tid < nch) {
+    if (kind == 3) {
+    } else if (tid < nch) {
       const int* sp = slots + ui * 8 + tid;
       int v;
       while ((v = ld_relaxed_gpu(sp)) == 0) __nanosleep(32);
@@ -735,7 +756,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     } else if (tid < kUnitTok && tid >= nch * kChunk) {
       tok[tid] = 0;                                      // padded rows (masked below)
     }
-    ntok = nch * kChunk;
+    ntok = kind == 0 ? nch * kChunk : min(kUnitTok, n_gen - ui * kUnitTok);
     if (early_next) pdl_trigger();                       // next layer's score may become resident
     trace(2, 2);
     __syncthreads();
@@ -792,7 +813,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
         }
       }
     }
-    if (dbg) {   // a4 parity hook: bf16 of the fp32 keys at the chunk's rank in the ascending selection
+    if (dbg && kind == 0) {   // a4 parity hook: bf16 of the fp32 keys at the chunk's rank in the ascending selection
       __syncthreads();                                   // A rows consumed: reuse their smem for the ids
       int* ids = reinterpret_cast<int*>(As);
       for (int i = tid; i < D.k; i += 256) {
@@ -878,7 +899,9 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       if (sub < 4 * HC) {
         const int i = sub / HC, hq = h0 + sub % HC, row = ty + 16 * i;
         // window unit: query row hq (token i = hq % s_q) sees new tokens 0..i only (causal, R28)
-        const bool vis = row < ntok && (kind != 2 || ui * kUnitTok + row < T_win - D.sq + 1 + hq % D.sq);
+        // (generated low-rank unit: token g = ui*64 + row likewise sees g <= step + i)
+        const bool vis = row < ntok && (kind == 0 || kind == 1 || (kind == 2 && lowrank) ||
+                                        ui * kUnitTok + row < (kind == 2 ? T_win - D.sq : stp0) + 1 + hq % D.sq);
         P[hq * kUnitTok + row] = vis ? pv[0] * scale : -INFINITY;
       }
     }
@@ -946,7 +969,7 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return base + o; };
   const int tph = tiles_per_head(D);
   const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
-  const int n_win_max = (D.wcap + kUnitTok - 1) / kUnitTok;
+  const int n_win_max = (D.wcap + kUnitTok - 1) / kUnitTok + 1;   // (+1: tail and generated units split, NEXT-4)
   const int n_split = n_sel_u + n_out_u + n_win_max;
   const size_t BHq = (size_t)D.b * D.hq, BHk = (size_t)D.b * D.hk;
   char* p_log = carve(BHq * D.n_c * 4);
@@ -1079,15 +1102,19 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     if (ev_sel && (e = cudaEventRecord(ev_sel, st))) return e;   // sub-batch pipelining: next chain may start
   }
   const int n_sel_u = (D.k + 7) / 8, n_out_u = (D.o * kChunk + kUnitTok - 1) / kUnitTok;
-  const int n_win_u = (D.w_eff + (D.step_dev ? D.max_step : step) + D.sq + kUnitTok - 1) / kUnitTok;
-  const int n_split = n_sel_u + n_out_u + n_win_u;
+  const int n_live = (D.step_dev ? D.max_step : step) + D.sq;   // generated tokens the grid is sized for
+  // plain window: one run of units over tail + generated; low-rank generated keys (NEXT-4): tail units
+  // (exact keys) + generated units (keys rebuilt from their rank-r rows)
+  const int n_win_u = D.lr_A ? (D.w_eff + kUnitTok - 1) / kUnitTok : (D.w_eff + n_live + kUnitTok - 1) / kUnitTok;
+  const int n_gen_u = D.lr_A ? (n_live + kUnitTok - 1) / kUnitTok : 0;
+  const int n_split = n_sel_u + n_out_u + n_win_u + n_gen_u;
   const int units = D.b * D.hk * n_split;
   // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score
   // grid then launches only when this grid drains)
   const int early_next = tuning().early_next;
   if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
                       ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
-                      n_sel_u, n_out_u, n_win_u, n_split, scale, dbg_keys, early_next))) return e;
+                      n_sel_u, n_out_u, n_win_u, n_gen_u, n_split, scale, dbg_keys, early_next))) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
   if (tuning().relay) {                                  // SKV_NO_RELAY=1 omits the relay grid
     if ((e = launch_pdl(k_relay, dim3(1), dim3(32), 0, st))) return e;
@@ -1191,6 +1218,7 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
     L.K_win = Ly.K_win + (size_t)r0 * hk * D.wcap * d;
     L.V_win = Ly.V_win + (size_t)r0 * hk * D.wcap * d;
     L.V_host = Ly.V_host + (size_t)r0 * hk * s * d;
+    if (D.lr_A) { Ds.lr_A = D.lr_A + (size_t)r0 * D.wcap * D.r; Ds.lr_B = L.B; }
     if (Ly.vc_dir) {
       L.vc_values = Ly.vc_values + (size_t)r0 * hk * 2 * D.k * kChunk * d;
       L.vc_dir = Ly.vc_dir + (size_t)r0 * hk * D.n_c;

@@ -15,6 +15,9 @@ struct Dims {          // validated, derived sizes
   int sq;              // s_q query tokens per call (rows of one q head are consecutive: hq*s_q + i)
   const int* lens;     // ragged batch: device int32 [b] per-request context lengths (nullable = all s);
                        // then s, n_c are the padded layout sizes and w_eff is the largest per-request w_eff
+  // low-rank generated keys (NEXT-4; nullable = plain window): the layer's B and its A_gen rows
+  const uint16_t* lr_B;
+  uint16_t* lr_A;      // [b][wcap][r]: row g = generated token g (decode step index)
 };
 #ifdef __CUDACC__
 // per-request sizes of a ragged batch (R8 applied to each request's own length)
@@ -38,6 +41,7 @@ struct Layer {
   int32_t* outlier_ids;
   uint16_t *K_out, *V_out, *K_win, *V_win;
   const uint16_t* V_host;
+  uint16_t* A_gen;                    // optional low-rank generated keys [b][wcap][r] (NEXT-4)
   // optional value-chunk cache (R26); all null = off
   uint16_t* vc_values;                // [b][hk][2][k*c][d]
   unsigned long long* vc_dir;         // [b][hk][n_c]  (tag << 32) | slot

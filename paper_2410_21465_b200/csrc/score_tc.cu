@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <cstdlib>
 
+#include "append.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -184,13 +185,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     }
   }
   const int stp = D.step_dev ? min(max(ld_acquire_gpu(D.step_dev), 0), D.max_step) : step;
-  for (int idx = blockIdx.x * kTcThreads + tid; idx < D.b * D.hk * D.sq * 32; idx += gridDim.x * kTcThreads) {
-    const int bhi = idx >> 5, arr = (idx >> 4) & 1, p = idx & 15;   // (b, h, new token i)
-    const int bh = bhi / D.sq, i = bhi - bh * D.sq;
-    const size_t dst = ((size_t)bh * D.wcap + req_weff(D, bh / D.hk) + stp + i) * kHeadDim + p * 8;
-    const uint16_t* src = (arr ? v_new : k_new) + (size_t)bhi * kHeadDim + p * 8;
-    *reinterpret_cast<uint4*>((arr ? V_win : K_win) + dst) = *reinterpret_cast<const uint4*>(src);
-  }
+  window_append(D, k_new, v_new, K_win, V_win, stp, blockIdx.x * kTcThreads + tid, gridDim.x * kTcThreads);
 #pragma unroll
   for (int u = 0; u < (kBChunks + kTcThreads - 1) / kTcThreads; ++u) {
     const int i = tid + u * kTcThreads;

@@ -71,7 +71,7 @@ class LayerState:
     """One layer's tensors for the whole per-GPU batch."""
 
     def __init__(self, shape: Shape, device="cuda", V_host: torch.Tensor | None = None,
-                 value_cache: bool = False):
+                 value_cache: bool = False, lowrank_gen: bool = False):
         self.shape = S = shape
         b, hk, d = S.batch, S.n_kv_heads, S.head_dim
         self.lens_host = self.lens_dev = None
@@ -94,6 +94,8 @@ class LayerState:
         self.V_host = V_host
         # optional GPU-resident value-chunk cache (skv_layer.vc_*, DESIGN R26): two slot buffers of
         # k chunks per (request, KV head), the chunk directory and the hit counters
+        # optional low-rank generated keys (skv_layer.A_gen, NEXT-4): one rank-r row per generated token
+        self.A_gen = torch.zeros(b, S.window_cap, S.rank, dtype=bf, device=device) if lowrank_gen else None
         self.vc_values = self.vc_dir = self.vc_stats = None
         if value_cache:
             self.vc_values = torch.empty(b, hk, 2, S.budget * S.chunk, d, dtype=bf, device=device)
@@ -102,7 +104,8 @@ class LayerState:
 
     def layer(self) -> bd.SkvLayer:
         return bd.layer_struct(self.A, self.B, self.landmarks, self.outlier_ids, self.K_out, self.V_out,
-                               self.K_win, self.V_win, self.V_host, self.vc_values, self.vc_dir, self.vc_stats)
+                               self.K_win, self.V_win, self.V_host, self.vc_values, self.vc_dir, self.vc_stats,
+                               self.A_gen)
 
     def cache_stats(self):
         """-> int64 [b][h_kv][4] {generation, -, hits in the last step, hits in total} (synchronises)."""

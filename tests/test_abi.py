@@ -27,7 +27,7 @@ def test_header_declares_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert bd.shadowkv_abi_version() == 4
+    assert bd.shadowkv_abi_version() == 5
 
 
 def _dims(**kw):
@@ -62,7 +62,7 @@ def test_invalid_dims_rejected(lib, kw, status, needle):
     assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(**kw))) == 0
     assert needle in lib.shadowkv_last_error().decode()
     rope = bd.SkvRope(128, 0, 16)
-    layer = bd.SkvLayer(*([16] * 9 + [None] * 3))
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 4))
     st = lib.shadowkv_decode_step(ctypes.byref(_dims(**kw)), ctypes.byref(rope), ctypes.byref(layer),
                                   16, 16, 16, 0, 16, None, None, 256, None)
     assert st == status
@@ -71,7 +71,7 @@ def test_invalid_dims_rejected(lib, kw, status, needle):
 def test_decode_argument_errors_before_any_cuda_call(lib):
     d = _dims()
     rope = bd.SkvRope(128, 0, 16)
-    layer = bd.SkvLayer(*([16] * 9 + [None] * 3))
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 4))
     call = lambda **kw: lib.shadowkv_decode_step(
         ctypes.byref(d), ctypes.byref(kw.get("rope", rope)), ctypes.byref(kw.get("layer", layer)),
         kw.get("q", 16), 16, 16, kw.get("step", 0), kw.get("out", 16), None, None, kw.get("ws", 256), None)
@@ -93,6 +93,8 @@ def test_decode_argument_errors_before_any_cuda_call(lib):
     assert call(layer=partial) == bd.SKV_EINVAL and "vc_" in lib.shadowkv_last_error().decode()
     misal = bd.SkvLayer(*([16] * 9 + [16, 24, 16]))
     assert call(layer=misal) == bd.SKV_EINVAL and "aligned" in lib.shadowkv_last_error().decode()
+    gen_misal = bd.SkvLayer(*([16] * 9 + [None, None, None, 24]))  # low-rank generated keys (NEXT-4)
+    assert call(layer=gen_misal) == bd.SKV_EINVAL and "A_gen" in lib.shadowkv_last_error().decode()
 
 
 def test_ctypes_layer_struct_matches_header(tmp_path):
@@ -145,7 +147,7 @@ def test_q_len_validation(lib):
     assert lib.shadowkv_workspace_bytes(ctypes.byref(_dims(q_len=2))) > lib.shadowkv_workspace_bytes(ctypes.byref(_dims()))
     d = _dims(q_len=4, window_cap=16 + 4)
     rope = bd.SkvRope(128, 0, 16)
-    layer = bd.SkvLayer(*([16] * 9 + [None] * 3))
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 4))
     call = lambda step: lib.shadowkv_decode_step(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(layer), 16, 16, 16,
                                                  step, 16, None, None, 256, None)
     assert call(1) == bd.SKV_EINVAL and "q_len" in lib.shadowkv_last_error().decode()   # 16 + 1 + 4 > 20
