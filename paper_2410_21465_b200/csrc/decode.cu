@@ -299,7 +299,8 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   if (early_trigger) pdl_trigger();                     // sparse-attn CTAs may start their prologue
   for (int i = tid; i < 256; i += NT) hist[i] = 0;
   if (tid == 0) { ccnt = 0; info[0] = 255; info[1] = 0; }   // B = 255 unless bins 0..254 reach k
-  pdl_wait();
+  cluster_arrive_relaxed();                             // #0: this CTA has started (waited on before the
+  pdl_wait();                                           //     first DSMEM store; long complete by then)
   trace(1, 1);
   int* fl = flags + bh * 4;
   if (crank == 0 && tid == 0) st_release_gpu(&fl[0], 1);  // score (incl. a7 window append) complete
@@ -362,6 +363,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   __syncthreads();                                                      // local histogram complete
   // push this rank's histogram into allhist[crank][.] of every rank (the release-arrive of barrier #1
   // orders these remote stores), so that after the barrier all histograms are local reads
+  cluster_wait_acquire();                               // #0: every CTA of the cluster has started
   if (tid < 256) {
     const int v = hist[tid];
 #pragma unroll
