@@ -36,9 +36,17 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 }
 
 // RoPE angle, R15: phi = fl32(fl32(t) * inv_freq) (no FMA contraction), accurate sincos.
+// RoPE angle phi = fl32(fl32(t) * inv_freq) (R15) and its sine / cosine.  Positions reach 2^20, so phi
+// reaches ~1e6 rad, where sincosf takes its slow (Payne-Hanek, local-memory) path.  phi is reduced
+// modulo 2 pi in fp64 instead (two-term 2 pi, |k| < 2^18: error < 1e-10 rad), then the fast path
+// hardware approximation runs on |r| <= pi (abs error < 1e-6, far inside the key tolerance, R23).
 __device__ __forceinline__ void rope_sincos(int t, float inv_freq, float* s, float* c) {
-  float phi = __fmul_rn((float)t, inv_freq);
-  sincosf(phi, s, c);
+  const float phi = __fmul_rn((float)t, inv_freq);
+  const double x = (double)phi;
+  const double k = rint(x * 0.15915494309189535);
+  double r = fma(-k, 6.283185307179586, x);
+  r = fma(-k, 2.4492935982947064e-16, r);
+  __sincosf((float)r, s, c);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

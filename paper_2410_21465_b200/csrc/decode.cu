@@ -552,12 +552,15 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
 struct AttnSmem {      // byte offsets into dynamic smem
   int v, a, bmat, q, p, tok, bytes;
 };
+constexpr int kKStride = kHeadDim + 4;            // fp32 key tile row stride (floats; +4 against bank conflicts)
 __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
   AttnSmem s;
   int off = 0;
   s.v = off; off += kUnitTok * kHeadDim * 2;                                 // V tile bf16
   s.a = off; { int ab = kUnitTok * r * 2; off += ab > kUnitTok * kHeadDim * 2 ? ab : kUnitTok * kHeadDim * 2; }  // A rows | K tile
-  s.bmat = off; off += r * kHeadDim * 2;                                    // B_h
+  s.bmat = off;                                                             // B_h; [a, bmat end) also holds
+  { const int bb = r * kHeadDim * 2, tile = kUnitTok * kKStride * 4 - (off - s.a);   // the fp32 rebuilt tile
+    off += bb > tile ? bb : tile; }
   s.q = off; off += G * kHeadDim * 4;                                       // q fp32
   s.p = off; off += G * kUnitTok * 4;                                       // logits / probs
   s.tok = off; off += kUnitTok * 4;
@@ -641,6 +644,45 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
       st[1] = 0; st[2] = hits; st[3] += hits; st[0] += 1;
     }
   }
+}
+
+// K~[64][128] = A_rows[64][r] . B_h[r][128]  (Alg 2 "MatMul(Gather(A, I), B)") with warp MMAs;
+// all 8 warps; result fp32 in Kt[64][kKStride], which aliases A_rows / B_h (synchronised here)
+__device__ __forceinline__ void rebuild_tile_mma(const uint16_t* As, const uint16_t* Bs, int r, float* Kt) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = (warp & 3) * 16, n0 = (warp >> 2) * 64;
+  float c[8][4];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.f;
+  const uint32_t a_base = smem_u32(As + (m0 + (lane & 15)) * r + (lane >> 4) * 8);
+  const uint32_t b_base = smem_u32(Bs + (lane & 15) * kHeadDim + n0 + (lane >> 4) * 8);
+  for (int k0 = 0; k0 < r; k0 += 16) {
+    uint32_t a[4];
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]) : "r"(a_base + k0 * 2));
+#pragma unroll
+    for (int nt = 0; nt < 8; nt += 2) {
+      uint32_t b[4];
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                   : "r"(b_base + (k0 * kHeadDim + nt * 8) * 2));
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2)
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                     "{%8, %9}, {%0, %1, %2, %3};"
+                     : "+f"(c[nt + h2][0]), "+f"(c[nt + h2][1]), "+f"(c[nt + h2][2]), "+f"(c[nt + h2][3])
+                     : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[2 * h2]), "r"(b[2 * h2 + 1]));
+    }
+  }
+  __syncthreads();                                       // every warp has read A rows and B_h
+  const int g = lane >> 2, cq = (lane & 3) * 2;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int col = n0 + t * 8 + cq;
+    *reinterpret_cast<float2*>(Kt + (m0 + g) * kKStride + col) = make_float2(c[t][0], c[t][1]);
+    *reinterpret_cast<float2*>(Kt + (m0 + g + 8) * kKStride + col) = make_float2(c[t][2], c[t][3]);
+  }
+  __syncthreads();
 }
 
 template <int G>
@@ -764,22 +806,18 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     __syncthreads();
     mbar_wait(&barAB, 0);
     trace(2, 3);
-    // ---- K~ = A_rows . B_h (fp32)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
-    const int r = D.r;
-    for (int rho = 0; rho < r; rho += 2) {
-      float b0[8], b1[8];
-      unpack8(*reinterpret_cast<const uint4*>(Bs + rho * kHeadDim + tx * 8), b0);
-      unpack8(*reinterpret_cast<const uint4*>(Bs + (rho + 1) * kHeadDim + tx * 8), b1);
+    // ---- K~ = A_rows . B_h on the tensor cores (bf16 x bf16 -> fp32, mma.sync m16n8k16): a 64 x 128 x r
+    //      GEMM per unit, warp w owns rows 16 (w % 4).., columns 64 (w / 4)..; the fp32 tile goes through
+    //      smem (over the consumed A rows / B_h) into the per-thread layout of the RoPE / logits code
+    {
+      float* Kt = reinterpret_cast<float*>(As);
+      rebuild_tile_mma(As, Bs, D.r, Kt);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(As + (ty + 16 * i) * r + rho);
-        const float a0 = bf_lo(a2), a1 = bf_hi(a2);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[i][e] = fmaf(a1, b1[e], fmaf(a0, b0[e], acc[i][e]));
+        const float4* src = reinterpret_cast<const float4*>(Kt + (ty + 16 * i) * kKStride + tx * 8);
+        const float4 v0 = src[0], v1 = src[1];
+        acc[i][0] = v0.x; acc[i][1] = v0.y; acc[i][2] = v0.z; acc[i][3] = v0.w;
+        acc[i][4] = v1.x; acc[i][5] = v1.y; acc[i][6] = v1.z; acc[i][7] = v1.w;
       }
     }
     // ---- RoPE at the tokens' absolute positions (R15), in registers
