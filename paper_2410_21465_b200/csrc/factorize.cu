@@ -6,7 +6,8 @@
 //   1. G = X^T X                      cuBLAS bf16 x bf16 -> fp32 GEMMs on tensor cores, one d x d
 //                                     block per (h, h') pair (X is h-blocked, not one strided matrix)
 //   2. G -> fp64, symmetrised         k_gram_to_f64
-//   3. G = V diag(lambda) V^T         cuSOLVER dsyevd (fp64; the D x D eigenproblem is independent of s)
+//   3. G = V diag(lambda) V^T         cuSOLVER dsyevdx, only the top r eigenpairs (fp64; the D x D
+//                                     eigenproblem is independent of s; SKV_FACT_EIG=full: dsyevd)
 //   4. W = top-r eigenvectors (sigma_i = sqrt(lambda_i), descending), B_h = W[h*d:(h+1)*d, :]^T
 //                                     k_take_top
 //   5. A = X W  (= U_r Sigma_r)       k_project: fp32 CUDA-core contraction of the bf16 keys with the
@@ -17,6 +18,7 @@
 #include <cublas_v2.h>
 #include <cusolverDn.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -32,10 +34,12 @@ __global__ void k_gram_to_f64(const float* __restrict__ G, double* __restrict__ 
 
 // W[(h,j)][rho] = eigenvector D-1-rho (dsyevd: ascending eigenvalues, vectors in columns);
 // sign fixed so the largest-|.| component is positive (deterministic factors; A.B is sign-free).
+// col0: the column of the largest eigenpair (eigenvalues ascend: D - 1 for the full solve, r - 1 for the
+// top-r range solve)
 __global__ void k_take_top(const double* __restrict__ V, const double* __restrict__ lam, int D, int r, int hk,
-                           float* __restrict__ W, uint16_t* __restrict__ B, float* __restrict__ sigma) {
+                           int col0, float* __restrict__ W, uint16_t* __restrict__ B, float* __restrict__ sigma) {
   const int rho = blockIdx.x;
-  const double* v = V + (size_t)(D - 1 - rho) * D;
+  const double* v = V + (size_t)(col0 - rho) * D;
   __shared__ double best_abs[32];
   __shared__ double best_val[32];
   double ba = -1.0, bv = 0.0;
@@ -54,7 +58,7 @@ __global__ void k_take_top(const double* __restrict__ V, const double* __restric
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
       if (best_abs[w] > ba || (best_abs[w] == ba && best_val[w] > bv)) { ba = best_abs[w]; bv = best_val[w]; }
     best_val[0] = bv;
-    if (sigma) sigma[rho] = (float)sqrt(fmax(lam[D - 1 - rho], 0.0));
+    if (sigma) sigma[rho] = (float)sqrt(fmax(lam[col0 - rho], 0.0));
   }
   __syncthreads();
   const double sg = best_val[0] < 0.0 ? -1.0 : 1.0;
@@ -178,11 +182,15 @@ FactorizeResult launch_factorize(int b, int hk, int d, int s, int r, const uint1
   if (cublasSetWorkspace(g_h.blas, ws.blas_ws, kFactorizeBlasWs) != CUBLAS_STATUS_SUCCESS) {
     res.err = cudaErrorUnknown; res.what = "cublasSetWorkspace"; return res;
   }
-  int lwork = 0;
-  if (cusolverDnDsyevd_bufferSize(g_h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, ws.Gd, D, ws.lam,
-                                  &lwork) != CUSOLVER_STATUS_SUCCESS) {
-    res.err = cudaErrorUnknown; res.what = "dsyevd_bufferSize"; return res;
-  }
+  int lwork = 0, meig = 0;
+  const char* ev = getenv("SKV_FACT_EIG");
+  const bool full = ev && ev[0] == 'f';                 // tuning / cross-check: the full eigensolve
+  const cusolverStatus_t qs = full
+      ? cusolverDnDsyevd_bufferSize(g_h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, ws.Gd, D, ws.lam,
+                                    &lwork)
+      : cusolverDnDsyevdx_bufferSize(g_h.solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER,
+                                     D, ws.Gd, D, 0.0, 0.0, D - r + 1, D, &meig, ws.lam, &lwork);
+  if (qs != CUSOLVER_STATUS_SUCCESS) { res.err = cudaErrorUnknown; res.what = "eigensolver bufferSize"; return res; }
   if ((size_t)lwork > ws.lwork) {
     res.err = cudaErrorInvalidValue; res.unused = lwork; res.what = "dsyevd needs more workspace"; return res;
   }
@@ -202,12 +210,14 @@ FactorizeResult launch_factorize(int b, int hk, int d, int s, int r, const uint1
     // 2. fp64, symmetrised
     k_gram_to_f64<<<(D * D + 255) / 256, 256, 0, st>>>(ws.G, ws.Gd, D);
     // 3. eigen-decomposition
-    if (cusolverDnDsyevd(g_h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, ws.Gd, D, ws.lam, ws.work,
-                         (int)ws.lwork, ws.info) != CUSOLVER_STATUS_SUCCESS) {
-      res.err = cudaErrorUnknown; res.what = "cusolverDnDsyevd"; return res;
-    }
+    const cusolverStatus_t es = full
+        ? cusolverDnDsyevd(g_h.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, ws.Gd, D, ws.lam, ws.work,
+                           (int)ws.lwork, ws.info)
+        : cusolverDnDsyevdx(g_h.solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER, D,
+                            ws.Gd, D, 0.0, 0.0, D - r + 1, D, &meig, ws.lam, ws.work, (int)ws.lwork, ws.info);
+    if (es != CUSOLVER_STATUS_SUCCESS) { res.err = cudaErrorUnknown; res.what = "eigensolver"; return res; }
     // 4. top-r eigenvectors -> W, B_h, sigma
-    k_take_top<<<r, 256, 0, st>>>(ws.Gd, ws.lam, D, r, hk, ws.W, B + (size_t)bi * hk * r * d,
+    k_take_top<<<r, 256, 0, st>>>(ws.Gd, ws.lam, D, r, hk, full ? D - 1 : r - 1, ws.W, B + (size_t)bi * hk * r * d,
                                   sigma ? sigma + (size_t)bi * r : nullptr);
     // 5. A = X W
     k_project<<<(s + kPT - 1) / kPT, 256, 0, st>>>(Kb, ws.W, A + (size_t)bi * s * r, s, hk, d, r);
