@@ -553,13 +553,15 @@ struct AttnSmem {      // byte offsets into dynamic smem
   int v, a, bmat, q, p, tok, bytes;
 };
 constexpr int kKStride = kHeadDim + 4;            // fp32 key tile row stride (floats; +4 against bank conflicts)
+constexpr int kBStride = kHeadDim + 8;            // B_h row stride in smem (bf16; 272 B rows: the 8 rows an
+                                                  // ldmatrix.trans phase reads fall in distinct banks)
 __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
   AttnSmem s;
   int off = 0;
   s.v = off; off += kUnitTok * kHeadDim * 2;                                 // V tile bf16
   s.a = off; { int ab = kUnitTok * r * 2; off += ab > kUnitTok * kHeadDim * 2 ? ab : kUnitTok * kHeadDim * 2; }  // A rows | K tile
   s.bmat = off;                                                             // B_h; [a, bmat end) also holds
-  { const int bb = r * kHeadDim * 2, tile = kUnitTok * kKStride * 4 - (off - s.a);   // the fp32 rebuilt tile
+  { const int bb = r * kBStride * 2, tile = kUnitTok * kKStride * 4 - (off - s.a);   // the fp32 rebuilt tile
     off += bb > tile ? bb : tile; }
   s.q = off; off += G * kHeadDim * 4;                                       // q fp32
   s.p = off; off += G * kUnitTok * 4;                                       // logits / probs
@@ -655,7 +657,7 @@ __device__ __forceinline__ void rebuild_tile_mma(const uint16_t* As, const uint1
 #pragma unroll
   for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.f;
   const uint32_t a_base = smem_u32(As + (m0 + (lane & 15)) * r + (lane >> 4) * 8);
-  const uint32_t b_base = smem_u32(Bs + (lane & 15) * kHeadDim + n0 + (lane >> 4) * 8);
+  const uint32_t b_base = smem_u32(Bs + (lane & 15) * kBStride + n0 + (lane >> 4) * 8);
   for (int k0 = 0; k0 < r; k0 += 16) {
     uint32_t a[4];
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -665,7 +667,7 @@ __device__ __forceinline__ void rebuild_tile_mma(const uint16_t* As, const uint1
       uint32_t b[4];
       asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
                    : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
-                   : "r"(b_base + (k0 * kHeadDim + nt * 8) * 2));
+                   : "r"(b_base + (k0 * kBStride + nt * 8) * 2));
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2)
         asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
@@ -738,6 +740,9 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   trace(2, 0);
   if (tid == 0) {   // selected-chunk units: one arrival per chunk-issuing thread
     mbar_init(&barAB, kind == 0 ? nch : 1); mbar_init(&barV, kind == 0 ? nch : 1); fence_mbar_init();
+    if (kind == 0 || kind == 3)                           // B_h's bytes, before any arrival can complete the phase
+      asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;"
+                   :: "r"(smem_u32(&barAB)), "r"((uint32_t)(D.r * kHeadDim * 2)) : "memory");
   }
   // q is a call input: stage it before waiting on the producer kernels
   for (int i = tid; i < G * kHeadDim; i += 256)
@@ -750,10 +755,13 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   float acc[4][8];
   if (kind == 0 || kind == 3) {
     const size_t bbytes = (size_t)D.r * kHeadDim * 2;
-    if (tid == 0) {   // B_h does not depend on the selection: fetch it before the PDL wait
-      asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&barAB)), "r"((uint32_t)bbytes) : "memory");
-      bulk_g2s(Bs, Ly.B + (size_t)bh * D.r * kHeadDim, (uint32_t)bbytes, &barAB);
-    }
+    // B_h does not depend on the selection: fetched before the PDL wait, one bulk copy per 256 B row into the
+    // padded layout, issued by warps 1..7 so that the chunk threads of warp 0 never queue behind them (the
+    // byte count was posted at barrier init, before any arrival)
+    (void)bbytes;
+    if (warp >= 1)
+      for (int i = tid - 32; i < D.r; i += 256 - 32)
+        bulk_g2s(Bs + i * kBStride, Ly.B + ((size_t)bh * D.r + i) * kHeadDim, kHeadDim * 2, &barAB);
     if (kind == 3) {  // generated tokens g0 .. g0+ntok-1: low-rank rows + values, positions s_b + g (R16)
       const int g0 = ui * kUnitTok, nt = min(kUnitTok, n_gen - g0);
       cta_wait_flag(&flags[(size_t)bh * 4]);                    // (score's a7 projection is visible)
