@@ -211,7 +211,7 @@ def cpu_baseline(cfg: synth.Config, seed: int, budget_s: float = 15.0):
     A, B, V = f(L["A"]), f(L["B"]), f(L["V"])
     n_c = (one.ctx_len - one.window_ctx) // one.chunk
     w_eff = one.ctx_len - n_c * one.chunk
-    st = O.build(A, B, V, inv, rot, il, one.chunk, one.n_outlier, one.window_ctx, w_eff + 1024)
+    st = O.build(A, B, V, inv, rot, il, one.chunk, one.n_outlier, one.window_ctx, w_eff + 1100)
     times, step = [], 0
     t_start = time.perf_counter()
     while time.perf_counter() - t_start < budget_s or len(times) < 2:
@@ -224,7 +224,26 @@ def cpu_baseline(cfg: synth.Config, seed: int, budget_s: float = 15.0):
         if step >= 1000:
             break
     t_layer = float(np.median(times))
+    # the same oracle with its BLAS pinned to one thread (a short bounded sample)
+    t1 = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            ts1 = []
+            t_start = time.perf_counter()
+            while (time.perf_counter() - t_start < budget_s / 3 or len(ts1) < 2) and len(ts1) < 50:
+                si = synth.gen_step(one, seed, 0, step)
+                t0 = time.perf_counter()
+                O.decode_step(st, A, B, V, f(si["q"]), f(si["k_new"]), f(si["v_new"]), step, one.budget, inv, rot,
+                              il, one.chunk)
+                ts1.append(time.perf_counter() - t0)
+                step += 1
+            t1 = float(np.median(ts1))
+    except Exception:  # noqa: BLE001
+        pass
     return {"value": 1.0 / (cfg.n_layers * t_layer), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1thread": (1.0 / (cfg.n_layers * t1)) if t1 else None,
+            "t_layer_ms_1thread": t1 * 1e3 if t1 else None,
             "sample": f"fp64 numpy oracle decode_step of 1 layer x 1 request at {one.ctx_len} ctx, {len(times)} steps, "
                       f"median {t_layer * 1e3:.1f} ms/layer, extrapolated x{cfg.n_layers} layers (state built untimed)",
             "t_layer_ms": t_layer * 1e3}
