@@ -518,11 +518,17 @@ def run_ours(args, cfg):
         raise SystemExit(f"{per_layer * 2 * n_states / 1e9:.1f} GB of pinned values exceed host RAM; "
                          f"use a smaller --layer-states")
     t_setup = time.perf_counter()
+    retried = False
     while True:                 # page-locking can fail below the RAM estimate: fewer states then
         try:
             pool = pinned_pool(per_layer * 2 * n_states)
             break
         except RuntimeError:
+            torch.cuda.cudart().cudaGetLastError()
+            if not retried:     # a previous process may still be releasing its pinned pages
+                retried = True
+                time.sleep(5)
+                continue
             if args.layer_states or n_states == 1:
                 raise
             n_states = max(1, n_states // 2)
