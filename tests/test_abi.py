@@ -165,3 +165,18 @@ def test_ragged_lengths_validation(lib):
         assert "ctx_lens[" in lib.shadowkv_last_error().decode()
     shortest = torch.tensor([4096, 16 + 8 * 12], dtype=torch.int32)
     assert lib.shadowkv_workspace_bytes(ctypes.byref(mk(shortest, 64))) > 0
+
+
+def test_shape_window_capacity_for_ragged_and_multi_query():
+    """Shape.from_config sizes the window for the largest per-request tail (R8 per request, R29) plus
+    steps x q_len generated tokens; dims() carries q_len and the length arrays."""
+    cfg = synth.CONFIGS["c1"].replace(batch=3)
+    lens = [4096, 3001, 2053]
+    sh = Shape.from_config(cfg, steps=5, q_len=2, ctx_lens=lens)
+    w_eff = [s - ((s - 16) // 8) * 8 for s in lens]
+    assert sh.window_cap == max(w_eff) + 10 and sh.q_len == 2 and sh.ctx_lens == tuple(lens)
+    import torch
+    lh = torch.tensor(lens, dtype=torch.int32)
+    d = sh.dims(lh, 64)
+    assert d.q_len == 2 and d.ctx_lens == lh.data_ptr() and d.ctx_lens_dev == 64
+    assert Shape.from_config(cfg, steps=5).window_cap == 16 + 5
