@@ -103,3 +103,50 @@ def test_ragged_batch_parity(name, q_len, value_cache):
             check_decode(one, f64(out[b:b + 1]), sel[b:b + 1].cpu().numpy(), f64(dbg[b:b + 1]), oo, os_, oz, ok)
     if value_cache:
         assert int(st.cache_stats()[..., 3].sum()) > 0, "drifting queries produced no cache hits"
+
+
+def test_ragged_graph_replay_matches_per_call():
+    """The graph-replayable entry point (device step counter) on a ragged batch with s_q = 2 and low-rank
+    generated keys: one captured graph replayed over three calls reproduces per-call decoding bit for bit."""
+    from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
+    cfg, lens, _ = CASES["llama_b3"]
+    q_len, calls, seed = 2, 3, 13
+    inp = synth.gen_layer(cfg, seed)
+    inv, rot, il = synth.rope_table(cfg)
+    shape = Shape.from_config(cfg, steps=calls, ctx_lens=lens, q_len=q_len)
+    rope = RopeTable(inv, rot, il)
+    ws = alloc_workspace(shape)
+    st = LayerState(shape, lowrank_gen=True)
+    st.A.copy_(inp["A"]); st.B.copy_(inp["B"]); st.V_host.copy_(inp["V"])
+    st.build(rope.struct, ws)
+    torch.cuda.synchronize()
+    win0 = (st.K_win.clone(), st.V_win.clone())
+    ins = []
+    for call in range(calls):
+        toks = [synth.gen_step(cfg, seed, 0, call * q_len + i) for i in range(q_len)]
+        ins.append({n: torch.stack([t[n] for t in toks], dim=2).cuda() for n in ("q", "k_new", "v_new")})
+    ref = []
+    for call, si in enumerate(ins):
+        out = torch.empty(si["q"].shape, dtype=torch.bfloat16, device="cuda")
+        st.decode(rope.struct, si["q"], si["k_new"], si["v_new"], call * q_len, out, ws)
+        torch.cuda.synchronize()
+        ref.append(out.clone())
+    st.K_win.copy_(win0[0]); st.V_win.copy_(win0[1]); st.A_gen.zero_()
+    qb, kb, vb = (ins[0][n].clone() for n in ("q", "k_new", "v_new"))
+    ob = torch.empty_like(ref[0])
+    step_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            st.decode_dev(rope.struct, qb, kb, vb, step_dev, (calls - 1) * q_len, ob, ws, stream=side)
+            step_dev.add_(q_len)
+        torch.cuda.synchronize()
+        step_dev.fill_(0)
+        st.K_win.copy_(win0[0]); st.V_win.copy_(win0[1]); st.A_gen.zero_()
+        torch.cuda.synchronize()
+        for call, si in enumerate(ins):
+            qb.copy_(si["q"]); kb.copy_(si["k_new"]); vb.copy_(si["v_new"])
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(ob, ref[call]), f"graph replay differs at call {call}"
