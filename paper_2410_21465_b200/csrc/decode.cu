@@ -1066,15 +1066,12 @@ __global__ void k_relay() { pdl_trigger(); }
 // SKV_SELECT_FALLBACK are read per call because tests toggle them inside one process
 struct Tuning {
   int early_sel, early_next, relay, merge_late;
-  int chain_stages, chain_sparse_smem;   // chained sub-batches: scorer ring depth, sparse CTA smem floor (bytes)
 };
 static const Tuning& tuning() {
   static const Tuning t = [] {
     auto is = [](const char* name, char c) { const char* v = getenv(name); return v && v[0] == c; };
-    auto num = [](const char* name, int dflt) { const char* v = getenv(name); return v ? atoi(v) : dflt; };
     return Tuning{is("SKV_EARLY_TRIGGER", '1') ? 1 : 0, is("SKV_SPARSE_TRIGGER", '0') ? 0 : 1,
-                  is("SKV_NO_RELAY", '1') ? 0 : 1, is("SKV_MERGE_TRIGGER", 'l') ? 1 : 0,
-                  num("SKV_CHAIN_STAGES", 0), num("SKV_CHAIN_SPARSE_KB", 0) * 1024};   // off: measured slower (DESIGN)
+                  is("SKV_NO_RELAY", '1') ? 0 : 1, is("SKV_MERGE_TRIGGER", 'l') ? 1 : 0};
   }();
   return t;
 }
@@ -1109,8 +1106,8 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (!attrs_set) {
     if ((e = cudaFuncSetAttribute(k_select<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSelectSmemMax))) return e;
-    const int sp_max = attn_smem_layout(256, G).bytes > 130 * 1024 ? attn_smem_layout(256, G).bytes : 130 * 1024;
-    if ((e = cudaFuncSetAttribute(k_sparse_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp_max))) return e;
+    if ((e = cudaFuncSetAttribute(k_sparse_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)attn_smem_layout(256, G).bytes))) return e;
     attrs_set = true;
   }
   const int tph = ws.n_sblk;
@@ -1123,8 +1120,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   const char* nt = getenv("SKV_NO_TC");                 // test hook: force the CUDA-core score
   e = (nt && nt[0] == '1') ? cudaErrorNotSupported
                            : launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
-                                                v_new, Ly.K_win, Ly.V_win, step, num_sms(), st,
-                                                D.chained ? tuning().chain_stages : 0);
+                                                v_new, Ly.K_win, Ly.V_win, step, num_sms(), st);
   if (prof && e == cudaSuccess) profile_mark(prof, kScore, false, st);
   if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
     cudaGetLastError();
@@ -1164,12 +1160,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score
   // grid then launches only when this grid drains)
   const int early_next = tuning().early_next;
-  // chained sub-batches: one sparse CTA per SM (a larger smem request), so that the next chain's scorer
-  // (a shallower ring) and selector find room on every SM while this chain streams its values
-  size_t sp_smem = (size_t)lay.bytes;
-  if (D.chained && (size_t)tuning().chain_sparse_smem > sp_smem)
-    sp_smem = (size_t)tuning().chain_sparse_smem < 130 * 1024 ? (size_t)tuning().chain_sparse_smem : 130 * 1024;
-  if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), sp_smem, st, D, R, Ly, q,
+  if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
                       ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
                       n_sel_u, n_out_u, n_win_u, n_gen_u, n_split, scale, dbg_keys, early_next))) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
@@ -1264,7 +1255,6 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
   for (int i = 0; i < n; ++i) {
     const int r0 = D.b * i / n, nb = D.b * (i + 1) / n - r0;
     Dims Ds = sub_dims(D, nb);
-    Ds.chained = 1;
     if (D.lens) Ds.lens = D.lens + r0;
     Layer L = Ly;
     L.A = Ly.A + (size_t)r0 * s * D.r;

@@ -18,7 +18,6 @@ struct Dims {          // validated, derived sizes
   // low-rank generated keys (NEXT-4; nullable = plain window): the layer's B and its A_gen rows
   const uint16_t* lr_B;
   uint16_t* lr_A;      // [b][wcap][r]: row g = generated token g (decode step index)
-  int chained;         // launched as one of several sub-batch chains (co-residency sizing, decode.cu)
 };
 #ifdef __CUDACC__
 // per-request sizes of a ragged batch (R8 applied to each request's own length)
@@ -107,7 +106,7 @@ template <int G>
 cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
                             float* logits, float2* part, int tiles_per_head, float scale,
                             const uint16_t* k_new, const uint16_t* v_new, uint16_t* K_win, uint16_t* V_win,
-                            int step, int n_sm, cudaStream_t st, int nst = 0);   // nst: ring stages (0 = max)
+                            int step, int n_sm, cudaStream_t st);
 
 // each returns cudaGetLastError() after its launches and adds to *launches
 cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* K_rope,

@@ -113,14 +113,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __restrict__ oids,
            const uint16_t* __restrict__ q, float* __restrict__ logits, float2* __restrict__ part,
            int tiles_per_head, float scale, const uint16_t* __restrict__ k_new,
-           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step, int early_trigger,
-           int nst) {                                                    // ring stages (<= kTcStages)
+           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step, int early_trigger) {
   static_assert(G <= 16, "N = 16 covers the GQA group");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
   uint8_t* sA = smem;                                          // [stages][32 KB]
-  uint8_t* sB = smem + nst * kTileBytes;                       // [kTcMaxHeads][4 KB]
+  uint8_t* sB = smem + kTcStages * kTileBytes;                 // [kTcMaxHeads][4 KB]
   __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], acc_full[kTcAcc], acc_empty[kTcAcc];
   __shared__ uint32_t tmem_base;
   __shared__ uint32_t obits[kTcMaxTiles * (kSTile / 32)];
@@ -138,7 +137,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   // the producer thread initialises the barriers and puts the first kTcStages tiles in flight
   // before anything else, so HBM streaming starts at kernel entry
   if (tid == 4 * 32 && ntile > 0) {
-    for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kTcStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < kTcAcc; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -150,7 +149,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   // landmarks are layer state written by build_cache, never by a decode-step kernel: the first ring
   // fills do not depend on the preceding grid and stream while it drains (PDL prologue)
   if (tid == 4 * 32 && ntile > 0) {
-    for (int i = 0; i < ntile && i < nst; ++i) {
+    for (int i = 0; i < ntile && i < kTcStages; ++i) {
       const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
       const int row0 = bh * D.n_c + tile * kSTile;
       mbar_expect_tx(&full[i], kTileBytes);
@@ -207,8 +206,8 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   if (warp == 4) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      for (int i = nst; i < ntile; ++i) {
-        const int s = i % nst, ph = (i / nst) & 1;
+      for (int i = kTcStages; i < ntile; ++i) {
+        const int s = i % kTcStages, ph = (i / kTcStages) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         const int t = t_begin + i, bh = t / tiles_per_head, tile = t - bh * tiles_per_head;
         const int row0 = bh * D.n_c + tile * kSTile;
@@ -222,7 +221,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     // (a single issuing thread is paced at ~70 cycles per tcgen05.mma; two overlap to the smem-read bound)
     if (lane == 0) {
       for (int i = warp - 5; i < ntile; i += 2) {
-        const int s = i % nst, ph = (i / nst) & 1, buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
+        const int s = i % kTcStages, ph = (i / kTcStages) & 1, buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
         mbar_wait(&full[s], ph);
         if (i < 4) trace_tc_any(trace_buf, 2 + i);                  // tile i landed in smem
         mbar_wait(&acc_empty[buf], aph ^ 1);
@@ -350,7 +349,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-size_t score_tc_smem_bytes(int nst) { return 1024 + (size_t)nst * kTileBytes + (size_t)kTcMaxHeads * kBBytes; }
+size_t score_tc_smem_bytes() { return 1024 + (size_t)kTcStages * kTileBytes + (size_t)kTcMaxHeads * kBBytes; }
 
 int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm) {
   const int total = D.b * D.hk * tiles_per_head;
@@ -368,9 +367,8 @@ template <int G>
 cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
                             float* logits, float2* part, int tiles_per_head, float scale,
                             const uint16_t* k_new, const uint16_t* v_new, uint16_t* K_win, uint16_t* V_win,
-                            int step, int n_sm, cudaStream_t st, int nst) {
+                            int step, int n_sm, cudaStream_t st) {
   auto enc = get_encode();
-  nst = nst < 1 ? kTcStages : (nst > kTcStages ? kTcStages : nst);
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap map;
   const cuuint64_t gdim[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)D.b * D.hk * D.n_c};
@@ -385,27 +383,27 @@ cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oid
   cudaError_t e;
   if (!attr) {
     if ((e = cudaFuncSetAttribute(k_score_tc<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)score_tc_smem_bytes(kTcStages)))) return e;
+                                  (int)score_tc_smem_bytes()))) return e;
     attr = true;
   }
   const int grid = score_tc_grid(D, tiles_per_head, n_sm);
   const char* et = getenv("SKV_EARLY_TRIGGER");            // tuning hook: 1 = PDL trigger at kernel start
   const int early = (et && et[0] == '1') ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(kTcThreads); cfg.dynamicSmemBytes = score_tc_smem_bytes(nst);
+  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(kTcThreads); cfg.dynamicSmemBytes = score_tc_smem_bytes();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;     // prologue overlaps the prior kernel
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at; cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_score_tc<G>, map, D, oids, q, logits, part, tiles_per_head, scale, k_new, v_new,
-                            K_win, V_win, step, early, nst);
+                            K_win, V_win, step, early);
 }
 
 #define SKV_INST(G)                                                                                       \
   template cudaError_t launch_score_tc<G>(const Dims&, const uint16_t*, const int32_t*, const uint16_t*,  \
                                           float*, float2*, int, float, const uint16_t*, const uint16_t*,  \
-                                          uint16_t*, uint16_t*, int, int, cudaStream_t, int);
+                                          uint16_t*, uint16_t*, int, int, cudaStream_t);
 SKV_INST(1)
 SKV_INST(2)
 SKV_INST(4)
