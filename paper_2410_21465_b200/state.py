@@ -52,7 +52,9 @@ class Shape:
         w_eff = s - ((s - w) // c) * c
         if ctx_lens is not None:
             ctx_lens = tuple(int(x) for x in ctx_lens)
-            w_eff = max(x - ((x - w) // c) * c for x in ctx_lens)
+            # the largest per-request tail; also the padded length's own (shape.dims() without the length
+            # arrays, e.g. for the workspace size, validates against it)
+            w_eff = max([w_eff] + [x - ((x - w) // c) * c for x in ctx_lens])
         return cls(cfg.batch if batch is None else batch, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, s,
                    cfg.rank, c, cfg.n_outlier, cfg.budget, w, w_eff + steps * q_len, q_len, ctx_lens)
 

@@ -180,3 +180,7 @@ def test_shape_window_capacity_for_ragged_and_multi_query():
     d = sh.dims(lh, 64)
     assert d.q_len == 2 and d.ctx_lens == lh.data_ptr() and d.ctx_lens_dev == 64
     assert Shape.from_config(cfg, steps=5).window_cap == 16 + 5
+    # the padded length's tail (4100: w_eff 20) also fits when every request has a shorter tail
+    wide = Shape.from_config(cfg.replace(ctx_len=4100), steps=1, ctx_lens=[4096, 2064, 1040])
+    assert wide.window_cap == 20 + 1
+    assert bd.shadowkv_workspace_bytes(wide.dims()) > 0
