@@ -1,22 +1,23 @@
-// Algorithm 2 "ShadowKV Decoding" + sparse attention on sm_100a (v2 pipeline).
+// Algorithm 2 "ShadowKV Decoding" + sparse attention on sm_100a.
 //
-//   k_score<G>        a7 window append; a1 logits l = <q, L_j>/sqrt(d).  Persistent CTAs stream
-//                     128-landmark tiles (32 KB, contiguous) HBM -> smem with cp.async.bulk through
-//                     a 4-stage mbarrier ring; half-warp per landmark row, transpose-reduce over the
-//                     16 lanes; per-tile softmax partials (max, sum exp) over landmarks only (R3).
-//   k_select<G>       a2 lse + z_j = max_group(l - lse) (R4, R5); a3 exact top-k:
-//                     z in smem, one bucket-histogram pass relative to z_max, exact resolution of the
-//                     threshold bucket (ties -> lower j, R12), ascending emit via block scan.
-//   k_sparse_attn<G>  a4+a5+a6 fused per unit of 8 chunks (64 tokens): the CTA first issues the
-//                     selected chunks' values host->smem with cp.async.bulk over PCIe, then
-//                     gathers the factor rows A[t], rebuilds K~ = A.B_h in fp32 registers,
-//                     applies RoPE with lane shuffles, computes q.K~ logits, and once the
-//                     values land does softmax + PV; outlier / window units read K,V from HBM.
-//                     The host fetch of every unit is in flight from the kernel's first
-//                     microseconds, so the key rebuild and attention math hide under it (the
-//                     paper's multi-stream overlap of P:40 / P:460, inside one grid).
-//                     The last unit of each (b, h) to finish (workspace counter) merges the
-//                     per-unit partials with a log-sum-exp combine and writes the bf16 output.
+//   k_score<G>        CUDA-core fallback of the tcgen05 scorer (score_tc.cu; SKV_NO_TC=1): a7 window
+//                     append, a1 logits l = <q, L_j>/sqrt(d) over 128-landmark tiles streamed through an
+//                     mbarrier ring, per-tile softmax partials over landmarks only (R3).
+//   k_select<G>       a2 lse + z_j = max_group log sum_i S (R4, R5; s_q rows per q head); a3
+//                     exact top-k on an 8-CTA cluster: bucket histogram relative to z_max (pushed
+//                     to every rank over DSMEM), definite chunks published unordered at deterministic slots,
+//                     the threshold bucket ranked exactly (ties -> lower j, R12); radix fallback.
+//   k_sparse_attn<G>  a4+a5+a6 fused per unit of <= 64 tokens.  Selected-chunk units: the thread owning a
+//                     chunk issues, the moment its slot is published, the chunk's factor rows A[t] (HBM,
+//                     P:182) and its 2 KB of values (cp.async.bulk from pinned host memory over PCIe, P:179;
+//                     or from the HBM value cache on a hit, R26).  K~ = A.B_h on the tensor cores
+//                     (mma.sync), RoPE, q.K~ logits, and once the values land softmax + PV.  Outlier
+//                     and window units read exact K, V from HBM; generated-token units (NEXT-4) rebuild
+//                     their keys from rank-r rows.  The host fetch is in flight from the kernel's first
+//                     microseconds, so rebuild and attention math hide under it (the paper's multi-stream
+//                     overlap of P:40 / P:460, inside one grid).
+//   k_relay, k_merge  the per-unit partials of each (b, q row) are combined by log-sum-exp into the bf16
+//                     output; the merge also closes the value cache's generation and re-zeroes the slots.
 // Kernels after the first are launched with programmatic dependent launch (PDL).
 #include <cstdlib>
 
@@ -775,8 +776,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     }
     // thread c < nch waits for its slot, then issues its chunk's two copies at once: the value fetch
     // of each chunk starts the moment k_select publishes it
-    if (kind == 3) {
-    } else if (tid < nch) {
+    if (kind == 0 && tid < nch) {                        // (generated units set their positions above)
       const int* sp = slots + ui * 8 + tid;
       int v;
       while ((v = ld_relaxed_gpu(sp)) == 0) __nanosleep(32);
@@ -805,7 +805,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       }
       mbar_expect_tx(&barV, kChunk * kHeadDim * 2);
       bulk_g2s(Vs + tid * kChunk * kHeadDim, vsrc, kChunk * kHeadDim * 2, &barV);
-    } else if (tid < kUnitTok && tid >= nch * kChunk) {
+    } else if (kind == 0 && tid < kUnitTok && tid >= nch * kChunk) {
       tok[tid] = 0;                                      // padded rows (masked below)
     }
     ntok = kind == 0 ? nch * kChunk : min(kUnitTok, n_gen - ui * kUnitTok);
