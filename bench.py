@@ -351,7 +351,7 @@ def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_by
     del g, layers, qd
     torch.cuda.empty_cache()
     from paper_2410_21465_b200 import shard
-    value = shard.job_tokens_per_s(b, ms / 1e3, device=dev)             # all ranks: sum tokens / max time
+    value = shard.job_tokens_per_s(args.tok_rank, ms / 1e3, device=dev)  # all ranks: sum tokens / max time
     return {"q_drift_rho": rho, "alpha": alpha, "value": value, "unit": UNIT, "ms_per_step": ms,
             "steps": steps, "warmup": warm, "host_bytes_per_layer": miss_bytes,
             "step_frac_of_host_roofline": t_roof / (ms * 1e-3),
@@ -417,7 +417,7 @@ def multi_query_leg(args, cfg, q_len, states, rope, seed, host_bytes, host_peak,
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    value = shard.job_tokens_per_s(b * q_len, ms / 1e3, device=dev)
+    value = shard.job_tokens_per_s(args.tok_rank * q_len, ms / 1e3, device=dev)
     del g, layers, ws
     torch.cuda.empty_cache()
     return {"q_len": q_len, "value": value, "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
@@ -473,7 +473,7 @@ def lowrank_gen_leg(args, cfg, states, rope, ws, seed, dev):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    value = shard.job_tokens_per_s(b, ms / 1e3, device=dev)
+    value = shard.job_tokens_per_s(args.tok_rank, ms / 1e3, device=dev)
     del g, layers
     torch.cuda.empty_cache()
     return {"value": value, "unit": UNIT, "ms_per_step": ms, "steps": steps, "warmup": warm,
@@ -492,12 +492,18 @@ def run_ours(args, cfg):
     from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace, binding as bd, shard
 
     dev = "cuda"
-    if args.scaling == "strong":
+    tok_rank = None                              # this rank's decode tokens per step (sums to the job's)
+    cfg0, strong_note = cfg, None
+    if args.scaling == "strong":                 # by request, or by KV head when batch < n
         pl = shard.plan(cfg.batch, cfg.n_q_heads, cfg.n_kv_heads, rank, world)
-        if pl.mode != "request":
-            raise SystemExit("strong scaling needs batch >= n_gpus")
-        cfg = cfg.replace(batch=pl.batch)
+        tok_rank = shard.tokens_this_rank(pl, cfg.n_kv_heads)
+        cfg = cfg.replace(batch=pl.batch, n_kv_heads=pl.n_kv_heads, n_q_heads=pl.n_q_heads)
+        strong_note = (f"strong scaling: {cfg0.batch} request(s) x {cfg0.n_kv_heads} KV heads split by {pl.mode} over "
+                       f"{world} GPU(s); no collective on the data path")
     Lm, b = cfg.n_layers, cfg.batch
+    if tok_rank is None:
+        tok_rank = float(b)
+    args.tok_rank = tok_rank
     n_total = args.warmup + 2 * args.steps + args.e2e_steps + 48
     shape = Shape.from_config(cfg, steps=n_total + 1)
     inv, rot, il = synth.rope_table(cfg)
@@ -606,7 +612,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
     gpu_launches = launches[0]
     ms_local = e0.elapsed_time(e1) / args.steps
-    value = shard.job_tokens_per_s(b, ms_local / 1e3, device=dev)        # sum tokens / max time
+    value = shard.job_tokens_per_s(tok_rank, ms_local / 1e3, device=dev)  # sum tokens / max time
     ms = shard.max_over_ranks(ms_local, device=dev)
 
     # --- dominant-kernel timing: a second timed pass of K steps with CUDA events recorded on the
@@ -648,7 +654,7 @@ def run_ours(args, cfg):
     f1.record(stream)
     torch.cuda.synchronize()
     e2e_local = f0.elapsed_time(f1) / max(1, args.e2e_steps)
-    e2e_value = shard.job_tokens_per_s(b, e2e_local / 1e3, device=dev)
+    e2e_value = shard.job_tokens_per_s(tok_rank, e2e_local / 1e3, device=dev)
     e2e_ms = shard.max_over_ranks(e2e_local, device=dev)
 
     # --- roofline of the dominant kernel (fused rebuild+gather+attention: host-link bound) -----
@@ -724,6 +730,9 @@ def run_ours(args, cfg):
             "clocks": clk.summary(),
             "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
             "setup_s": setup_s}
+    if strong_note:                              # the job's batch, not the per-rank share
+        line["config"].update(global_batch=cfg0.batch, parallelism=strong_note,
+                              per_rank={"batch": cfg.batch, "n_kv_heads": cfg.n_kv_heads, "n_q_heads": cfg.n_q_heads})
     if value_cache:
         line["value_cache"] = value_cache[0] if len(value_cache) == 1 else value_cache
     if multi_query:

@@ -59,6 +59,12 @@ def plan(batch: int, n_q_heads: int, n_kv_heads: int, rank: int, world: int) -> 
     return Plan("kv_head", (0, 1), h, (h[0] * g, h[1] * g))
 
 
+def tokens_this_rank(p: Plan, n_kv_heads: int) -> float:
+    """This rank's share of the job's decode tokens per step: its requests, or, under KV-head sharding,
+    the fraction of the request's heads it computes (the ranks' shares sum to the batch)."""
+    return p.batch * p.n_kv_heads / n_kv_heads
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Step time of the whole job = the slowest rank (timing rule)."""
     import torch.distributed as dist

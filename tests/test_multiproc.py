@@ -70,3 +70,13 @@ def test_two_rank_job_throughput_gloo():
         assert abs(tmax - 0.015) < 1e-12
         assert abs(tps - 64 / 0.015) < 1e-6
     assert [r[2] for r in res] == [0.0, 32.0]
+
+
+def test_tokens_per_rank_sum_to_the_batch():
+    """Request sharding: each rank's requests; KV-head sharding (batch < world): each rank's fraction of the
+    request's heads; either way the shares sum to the job's batch (bench.py's strong-scaling tokens/s)."""
+    for batch, hq, hk, world in [(64, 32, 8, 8), (64, 32, 8, 3), (1, 32, 8, 4), (1, 32, 8, 8), (1, 32, 2, 2)]:
+        shares = [shard.tokens_this_rank(shard.plan(batch, hq, hk, r, world), hk) for r in range(world)]
+        assert abs(sum(shares) - batch) < 1e-12
+        if batch < world:
+            assert all(abs(x - 1.0 / world) < 1e-12 for x in shares) or hk % world
