@@ -154,14 +154,17 @@ SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *ro
 /* One decode step of Algorithm 2 for the whole batch, on `stream`:
  *   a7  K_win/V_win slot w_eff+step <- k_new, v_new (Alg 2 input K, V; R18)
  *   a1  l_{hq,j} = <q_hq, L_{h,j}> / sqrt(d) over landmarks j (R6)
- *   a2  z_{h,j} = max_{hq in group h} (l_{hq,j} - logsumexp_j l_{hq,.})  (= log S2, R4, R5)
+ *   a2  z_{h,j} = max_{hq in group h} log sum_{i < s_q} softmax_j(l_{hq,i,.})_j  (= log S2, P:169-172,
+ *       R4, R5; for s_q = 1: max_hq (l_{hq,j} - logsumexp_j l_{hq,.}))
  *   a3  I_h = ArgTopK(z_h, k), ties -> lower chunk id, ascending (R12)
  *   a4  K~ = RoPE_t(A[t] . B_h) for the k*c tokens of I_h at their absolute positions
  *   a5  V~ = V_host rows of those tokens, gathered zero-copy over the host link; with a
  *       value cache, chunks selected in the previous step are copied from vc_values instead, and
  *       every selected chunk is written to this step's slot buffer (R26)
- *   a6  out_hq = softmax attention of q_hq over outlier tokens + K~/V~ + window slots
- *       [0, w_eff+step] (R17)
+ *   a6  out_{hq,i} = softmax attention of query token i over outlier tokens + K~/V~ + window slots
+ *       [0, w_eff+step+i] (R17; causal among the new tokens, R28)
+ * Ragged batches (dims.ctx_lens): s, w_eff, positions and the chunk grid are per request (R29).
+ * Low-rank generated keys (layer.A_gen): generated tokens are attended with RoPE_t(A_gen[g] . B_h) (R30).
  * q      device bf16 [b][h_q][s_q][d], token i post-RoPE at position s+step+i (R16)
  * k_new  device bf16 [b][h_kv][s_q][d] post-RoPE (pre-RoPE with layer.A_gen);  v_new [b][h_kv][s_q][d]
  *        (written to window slots w_eff+step .. w_eff+step+s_q-1; the next call's step is step+s_q)
