@@ -691,18 +691,29 @@ def run_ours(args, cfg):
     selection = {"mean_run_length_chunks": float(sum(runs) / len(runs)), "chunks_per_kv_head": cfg.budget,
                  "sample": f"{len(runs)} (layer, request, KV head) selections at the last step index"}
 
+    def leg(fn, *a):
+        """A widened-row leg never costs the headline line on one GPU: a failure is reported in its place.
+        (With N > 1 the legs' collectives must stay in step across ranks, so errors propagate.)"""
+        if world > 1:
+            return fn(*a)
+        try:
+            return fn(*a)
+        except Exception as e:  # noqa: BLE001
+            torch.cuda.synchronize()
+            return {"error": f"{type(e).__name__}: {e}"[:300]}
+
     value_cache = None
     if args.vc_rho:
-        value_cache = [value_cache_leg(args, cfg, float(r), states, rope, ws, out, stream, seed, host_bytes, host_peak,
-                                       n_total, dev) for r in args.vc_rho.split(",") if r.strip()]
+        value_cache = [leg(value_cache_leg, args, cfg, float(r), states, rope, ws, out, stream, seed, host_bytes,
+                           host_peak, n_total, dev) for r in args.vc_rho.split(",") if r.strip()]
 
     multi_query = None
     if args.q_len_leg and args.q_len_leg > 1:
-        multi_query = multi_query_leg(args, cfg, args.q_len_leg, states, rope, seed, host_bytes, host_peak, dev)
+        multi_query = leg(multi_query_leg, args, cfg, args.q_len_leg, states, rope, seed, host_bytes, host_peak, dev)
 
     lowrank_gen = None
     if args.lowrank_gen_leg:
-        lowrank_gen = lowrank_gen_leg(args, cfg, states, rope, ws, seed, dev)
+        lowrank_gen = leg(lowrank_gen_leg, args, cfg, states, rope, ws, seed, dev)
 
     breakdown = None
     if args.breakdown:
