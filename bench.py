@@ -352,7 +352,17 @@ def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_by
     torch.cuda.empty_cache()
     from paper_2410_21465_b200 import shard
     value = shard.job_tokens_per_s(args.tok_rank, ms / 1e3, device=dev)  # all ranks: sum tokens / max time
+    # P:200-206 equivalent bandwidth: the dense-attention KV bytes a layer would read (2 S M per KV head,
+    # M = d * 2 B) over the measured layer time, and the paper's analytic B_eq at the measured alpha with
+    # this box's bandwidths (HBM from MEASURED_PEAKS.json, host link measured live)
+    hbm_gbs, _ = load_peaks()
+    S, C, K, O = cfg.ctx_len, cfg.chunk, cfg.budget, cfg.n_outlier
+    dense_bytes = 2.0 * S * cfg.head_dim * 2 * cfg.n_kv_heads * b
+    beq_model = 2.0 * S * hbm_gbs / (S / C + 2.0 * (K + O) * C + (1.0 - alpha) * K * C * hbm_gbs / host_peak)
+    beq_meas = dense_bytes / (ms * 1e-3 / Lm) / 1e9
     return {"q_drift_rho": rho, "alpha": alpha, "value": value, "unit": UNIT, "ms_per_step": ms,
+            "equivalent_bandwidth_GBps": {"measured": beq_meas, "paper_model_P204": beq_model, "hbm_peak": hbm_gbs,
+                                          "host_peak": host_peak},
             "steps": steps, "warmup": warm, "host_bytes_per_layer": miss_bytes,
             "step_frac_of_host_roofline": t_roof / (ms * 1e-3),
             "note": "P:156 cache-aware decode: chunks selected in the previous step come from HBM (capacity k, "
@@ -741,6 +751,14 @@ def run_ours(args, cfg):
             "clocks": clk.summary(),
             "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
             "setup_s": setup_s}
+    # P:200-206 equivalent bandwidth of the uncached step (alpha = 0): dense KV bytes / layer time, and the
+    # paper's model with this box's bandwidths
+    S_, C_, K_, O_ = cfg.ctx_len, cfg.chunk, cfg.budget, cfg.n_outlier
+    dense_b = 2.0 * S_ * cfg.head_dim * 2 * cfg.n_kv_heads * b
+    line["equivalent_bandwidth_GBps"] = {
+        "measured": dense_b / (ms * 1e-3 / Lm) / 1e9,
+        "paper_model_P204": 2.0 * S_ * hbm_peak / (S_ / C_ + 2.0 * (K_ + O_) * C_ + K_ * C_ * hbm_peak / host_peak),
+        "note": "dense-attention KV bytes per layer over the measured layer time (P:200-206); alpha = 0 here"}
     if strong_note:                              # the job's batch, not the per-rank share
         line["config"].update(global_batch=cfg0.batch, parallelism=strong_note,
                               per_rank={"batch": cfg.batch, "n_kv_heads": cfg.n_kv_heads, "n_q_heads": cfg.n_q_heads})
