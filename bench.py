@@ -49,8 +49,12 @@ def parse():
     ap.add_argument("--graph", choices=["on", "off"], default="on",
                     help="time CUDA-graph replays of the 32-layer step (shadowkv_decode_step_dev, device-side step "
                          "counter) instead of per-call stream launches")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="weak: every rank runs the config's batch; strong: the batch is split over ranks")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="weak: every rank runs the config's batch; strong: the batch is split over ranks "
+                         "(default: strong for c3, whose 64 requests SURVEY 8(d) splits 64/n, weak otherwise)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: gloo process group, shard plan and max-over-ranks timing of an empty step "
+                         "(tests the multi-rank launch path on CPU)")
     ap.add_argument("--vc-rho", default="0.95",
                     help="value-cache leg (P:156, DESIGN R26/R27): comma list of query-drift correlations rho; "
                          "each runs the same step with a GPU value cache per layer and drifting queries and "
@@ -72,8 +76,13 @@ def dist_env():
     return rank, world, local
 
 
+MODEL_SHAPE = {"c1": "Llama-3.1-8B-shape (one layer)", "c2": "Llama-3.1-8B-shape", "c3": "Llama-3.1-8B-shape",
+               "c4": "Llama-3-8B-1M-shape", "c5": "GLM-4-9B-1M-shape (32 q / 2 KV heads)"}
+
+
 def workload_config(cfg: synth.Config, n_gpus: int) -> dict:
-    return {"workload": f"{cfg.name}: Llama-3.1-8B-shape decode attention, {cfg.n_layers} layers, batch "
+    shape = MODEL_SHAPE.get(cfg.name, f"{cfg.n_q_heads} q / {cfg.n_kv_heads} KV heads")
+    return {"workload": f"{cfg.name}: {shape} decode attention, {cfg.n_layers} layers, batch "
                         f"{cfg.batch}/GPU, {cfg.ctx_len} ctx, rank {cfg.rank}, chunk {cfg.chunk}, "
                         f"{cfg.n_outlier} outlier chunks, k={cfg.budget} chunks (1.56%), window {cfg.window_ctx}",
             "n_q_heads": cfg.n_q_heads, "n_kv_heads": cfg.n_kv_heads, "head_dim": cfg.head_dim,
@@ -162,18 +171,30 @@ def pinned_pool(nbytes: int) -> torch.Tensor:
     return buf
 
 
-def measure_dma_h2d(pool: torch.Tensor) -> float:
-    """Pinned host->device copy-engine bandwidth, 1 GiB, best of 5 (GB/s)."""
+def measure_dma_h2d(pool: torch.Tensor, world: int = 1):
+    """Pinned host->device copy-engine bandwidth B_host(n), 1 GiB, best of 6 (GB/s).  With n ranks every
+    rank copies at the same time (a barrier before each repetition), so the figure is the per-GPU
+    bandwidth while all n GPUs pull from host DRAM concurrently; returns
+    (this rank's GB/s, every rank's GB/s)."""
     n = min(pool.numel(), 1 << 29)
     src = pool[:n]
     dst = torch.empty(n, dtype=pool.dtype, device="cuda")
     best = 1e30
     for _ in range(6):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(); dst.copy_(src, non_blocking=True); e1.record(); e1.synchronize()
         best = min(best, e0.elapsed_time(e1))
     del dst
-    return n * 2 / best / 1e6
+    own = n * 2 / best / 1e6
+    if world > 1:
+        t = torch.zeros(world, dtype=torch.float64, device="cuda")
+        t[torch.distributed.get_rank()] = own
+        torch.distributed.all_reduce(t)
+        return own, [float(x) for x in t.cpu()]
+    return own, [own]
 
 
 def load_peaks():
@@ -251,6 +272,13 @@ def cpu_baseline(cfg: synth.Config, seed: int, budget_s: float = 15.0):
 
 # ------------------------------------------------------------------------------------------------
 def run_reference(args, cfg):
+    """The oracle as it stands (fp64 numpy, oracle/) on the box's host cores, on this arm's config,
+    metric and unit.  One step = every layer of one request: for c2 (batch 1) that is the whole
+    workload step, measured as is; for the batched configs one request's layers are the bounded
+    sample and tokens/s counts that one request.  One layer state is built (untimed) and serves
+    every layer's decode call with that layer's own fresh q / k_new / v_new (32 distinct states would
+    only lengthen the untimed setup: the oracle's per-layer working set, ~0.3 GB, is far beyond the
+    CPU caches either way)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -266,24 +294,32 @@ def run_reference(args, cfg):
     inv, rot, il = synth.rope_table(one)
     f = lambda t: t.to(torch.float64).numpy()
     A, B, V = f(L["A"]), f(L["B"]), f(L["V"])
-    n_c = (one.ctx_len - one.window_ctx) // one.chunk
-    w_eff = one.ctx_len - n_c * one.chunk
-    st = O.build(A, B, V, inv, rot, il, one.chunk, one.n_outlier, one.window_ctx, w_eff + args.warmup + args.steps + 2)
-    def one_step(i):
-        si = synth.gen_step(one, args.seed, 0, i)
-        return O.decode_step(st, A, B, V, f(si["q"]), f(si["k_new"]), f(si["v_new"]), i, one.budget, inv, rot, il,
-                             one.chunk)
+    n_steps = args.warmup + args.steps
+    st = O.build(A, B, V, inv, rot, il, one.chunk, one.n_outlier, one.window_ctx,
+                 (one.ctx_len - ((one.ctx_len - one.window_ctx) // one.chunk) * one.chunk) + n_steps + 2)
+    Lm = cfg.n_layers
+
+    def one_step(i):                       # all Lm layers of one request at decode step i
+        for l in range(Lm):
+            si = synth.gen_step(one, args.seed, l, i)
+            O.decode_step(st, A, B, V, f(si["q"]), f(si["k_new"]), f(si["v_new"]), i, one.budget, inv, rot, il,
+                          one.chunk)
+
     for i in range(args.warmup):
         one_step(i)
     t0 = time.perf_counter()
-    for i in range(args.warmup, args.warmup + args.steps):
+    for i in range(args.warmup, n_steps):
         one_step(i)
-    t_layer = (time.perf_counter() - t0) / args.steps
-    value = 1.0 / (cfg.n_layers * t_layer)          # one request's decode tokens/s on the host cores
-    sample = (f"each step = fp64 numpy oracle decode_step of 1 layer x 1 request of {cfg.name} "
-              f"({one.ctx_len} ctx); tokens/s extrapolated x{cfg.n_layers} layers")
+    ms_step = (time.perf_counter() - t0) / max(args.steps, 1) * 1e3
+    value = 1.0 / (ms_step / 1e3)                   # one request's decode tokens per second
+    whole = cfg.batch == 1
+    sample = (f"each step = fp64 numpy oracle decode_step for all {Lm} layers of 1 request of {cfg.name} "
+              f"({one.ctx_len} ctx, k={one.budget}); " +
+              ("this is the whole workload step (batch 1)" if whole else
+               f"a bounded sample of the {cfg.batch}-request step: tokens/s counts this one request") +
+              "; one untimed layer state serves every layer's call")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_layer * cfg.n_layers * cfg.batch * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth/)",
             "config": workload_config(cfg, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
@@ -671,7 +707,7 @@ def run_ours(args, cfg):
     g_ms, g_cnt = prof["sparse_attn"]
     g_avg_ms = g_ms / max(g_cnt, 1)
     host_bytes = b * cfg.n_kv_heads * cfg.budget * cfg.chunk * cfg.head_dim * 2          # HOST_alg per launch
-    host_peak = measure_dma_h2d(pool)
+    host_peak, host_all = measure_dma_h2d(pool, world)
     achieved = host_bytes / (g_avg_ms * 1e-3) / 1e9
     nt = load_ncu_traffic()
     same = nt.get("config", "c2") == cfg.name and world == 1 and args.scaling == "weak"
@@ -685,8 +721,10 @@ def run_ours(args, cfg):
                 "algorithmic_bytes_per_launch": host_bytes, "avg_launch_ms": g_avg_ms, "launches": g_cnt,
                 "share_of_step": g_ms / (prof_pass_ms * args.steps), "timing_pass_ms_per_step": prof_pass_ms,
                 "step_frac_of_roofline": (Lm * host_bytes / (host_peak * 1e9)) / (ms * 1e-3),
-                "peak_note": "pinned H2D copy-engine bandwidth measured live in this run (1 GiB, best of 6); "
-                             "zero-copy SM loads saturate ~51 GB/s (profiles/r01_probe_hostlink.txt)"}
+                "peak_note": "pinned H2D copy-engine bandwidth measured live in this run (1 GiB, best of 6; with N "
+                             "ranks all copy concurrently: B_host(n), this rank's share); zero-copy SM loads "
+                             "saturate ~51 GB/s (profiles/r01_probe_hostlink.txt)",
+                "host_link_concurrent_GBps": {"per_rank": host_all, "aggregate": sum(host_all), "n": world}}
 
     # --- selection adjacency: mean run length of consecutive selected chunk ids, so that
     #     contiguity is not silently helping the host link (2 KB pieces are fetched independently anyway)
@@ -777,10 +815,65 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per GPU) on this node through
+    torch.distributed.run with the same arguments, rendezvous on 127.0.0.1."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, cfg):
+    """--dry-run: the multi-rank path without a GPU -- gloo group, this rank's shard plan, an empty timed
+    step bracketed by barriers, max over ranks; rank 0 prints the plan of every rank."""
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    from paper_2410_21465_b200 import shard
+    pl = shard.plan(cfg.batch, cfg.n_q_heads, cfg.n_kv_heads, rank, world) if args.scaling == "strong" else \
+        shard.Plan("request", (0, cfg.batch), (0, cfg.n_kv_heads), (0, cfg.n_q_heads))
+    tok = shard.tokens_this_rank(pl, cfg.n_kv_heads)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    ms = shard.max_over_ranks((time.perf_counter() - t0) * 1e3)
+    plans = [None] * world
+    if world > 1:
+        dist.all_gather_object(plans, {"rank": rank, "mode": pl.mode, "requests": pl.requests,
+                                       "kv_heads": pl.kv_heads, "q_heads": pl.q_heads, "tokens": tok})
+    else:
+        plans = [{"rank": 0, "mode": pl.mode, "requests": pl.requests, "kv_heads": pl.kv_heads,
+                  "q_heads": pl.q_heads, "tokens": tok}]
+    total = shard.sum_over_ranks(tok)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "world_size": world, "scaling": args.scaling,
+                          "config": workload_config(cfg, world), "tokens_per_step": total, "ms_per_step": ms,
+                          "ranks": plans}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     cfg = synth.CONFIGS[args.config]
-    if args.impl == "reference":
+    if args.scaling is None:
+        args.scaling = "strong" if cfg.name == "c3" else "weak"
+    rank, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.dry_run:
+        run_dry(args, cfg)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_ours(args, cfg)

@@ -22,7 +22,21 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).
  *   - Errors: the call validates its arguments on the host before enqueuing anything.  On a
  *     non-OK status nothing was enqueued and shadowkv_last_error() (thread-local) explains why.
- *     Faults inside kernels surface at the caller's next synchronisation.
+ *     Faults inside kernels surface at the caller's next synchronisation -- or, with the
+ *     environment variable SKV_DEBUG_SYNC=1, as SKV_ECUDA of the call itself (every enqueuing call
+ *     then synchronises its stream, except while the stream is being captured into a graph).
+ *   - Setup: shadowkv_init(device) once per device before any build / decode call on it.  It creates
+ *     and configures everything the calls would otherwise set up on first use (kernel attributes,
+ *     internal streams and events, the tensor-map encoder), so build / decode never allocate, and a
+ *     device that was not initialised gives SKV_ESTATE.
+ *   - Ordering: decode_step's first kernel is launched with programmatic dependent launch and reads
+ *     the layer's landmarks and outlier_ids before it waits on the preceding kernel of `stream`.
+ *     If you rewrite those two arrays with your own KERNEL, do not enqueue decode_step directly after
+ *     it (put any other stream operation in between, e.g. an event record, or a build_cache: its last
+ *     kernel writes nothing).  Copies (cudaMemcpyAsync) are fully ordered.
+ *   - Debug: SKV_SERIALIZE=1 runs the decode kernels without overlap (no PDL, values before the key
+ *     rebuild); outputs are bit-identical to the overlapped schedule.  NVTX ranges name each ABI call
+ *     and each kernel launch (skv::score, skv::select, skv::sparse_attn, skv::merge).
  *
  * Symbols: b batch, h_q / h_kv query / KV heads (g = h_q / h_kv, q head hq uses KV head
  * floor(hq/g), R2), d = head_dim, s = ctx_len, r = rank, c = chunk, o = n_outlier, k = budget,
@@ -39,7 +53,7 @@
 extern "C" {
 #endif
 
-#define SHADOWKV_ABI_VERSION 5
+#define SHADOWKV_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define SKV_API __attribute__((visibility("default")))
@@ -52,7 +66,7 @@ typedef enum {
   SKV_EINVAL = 1,        /* bad argument (null pointer, size out of range, window overflow) */
   SKV_EUNSUPPORTED = 2,  /* valid per the paper but not compiled: d != 128, c != 8, g not in {1,2,4,8,16} */
   SKV_ECUDA = 3,         /* a CUDA runtime call or kernel launch failed */
-  SKV_ESTATE = 4         /* V_host is not page-locked + device-mapped */
+  SKV_ESTATE = 4         /* V_host is not page-locked + device-mapped; shadowkv_init not called */
 } skv_status;
 
 typedef struct {
@@ -131,6 +145,28 @@ typedef struct {
   uint16_t *A_gen;          /* device bf16 [b][window_cap][r]                                    */
 } skv_layer;
 
+/* One-time setup for `device` (idempotent, thread-safe): kernel shared-memory attributes for every
+ * compiled GQA group, the SM count, 8 high-priority internal streams + 16 events for the sub-batch
+ * chains of large batches, and the driver's cuTensorMapEncodeTiled.  Required before build / decode
+ * on that device (SKV_ESTATE otherwise); SKV_ECUDA if any of it fails.  Leaves the current device
+ * unchanged. */
+SKV_API skv_status shadowkv_init(int32_t device);
+
+/* Launch plan of the tcgen05 landmark scorer (a1) for these dims on a GPU with n_sm SMs, pure host
+ * arithmetic: plan[0] grid (CTAs), plan[1] tiles (128 landmarks) per CTA, plan[2] KV heads a CTA's
+ * tile range may touch, plan[3] CTAs per KV head (softmax partial slots used by the selector).
+ * SKV_EUNSUPPORTED when no grid satisfies the kernel's limits (<= 256 tiles and <= 4 KV heads per
+ * CTA, <= 64 partial slots per KV head), e.g. one request of ~8M tokens with 8 KV heads; decode_step
+ * returns the same status for such dims. */
+SKV_API skv_status shadowkv_score_plan(const skv_dims *dims, int32_t n_sm, int32_t *plan);
+
+/* Diagnostic: sin / cos of the RoPE angle phi = fl32(fl32(pos[p]) * inv_freq[i]) exactly as the
+ * decode kernels compute them (R15: fp64 reduction mod 2 pi, then the hardware sincos on |r| <= pi),
+ * for p < n, i < rotary_dim/2.  pos: device int32 [n]; sincos: device fp32 [n][rotary_dim/2][2]
+ * (sin, cos).  Asynchronous on `stream`. */
+SKV_API skv_status shadowkv_rope_sincos(const skv_rope *rope, const int32_t *pos, int32_t n, float *sincos,
+                                        void *stream);
+
 /* Bytes of scratch `workspace` (device, 256-byte aligned) that build_cache and decode_step need
  * for these dims.  Returns 0 on invalid dims (see shadowkv_last_error). Pure host arithmetic.
  * The workspace must be ZERO-FILLED once before its first use (it holds per-(request, KV head)
@@ -171,11 +207,14 @@ SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *ro
  * out    device bf16 [b][h_q][s_q][d]
  * sel_ids   nullable device int32 [b][h_kv][k]  -- parity hook for a3
  * dbg_keys  nullable device bf16 [b][h_kv][k*c][d] -- parity hook for a4 (rebuilt, post-RoPE)
- * Requires window_cap >= w_eff + step + s_q (SKV_EINVAL otherwise).
+ * Requires window_cap >= w_eff + step + s_q (SKV_EINVAL otherwise); SKV_EUNSUPPORTED when the
+ * scorer has no launch plan for the dims (shadowkv_score_plan).
  * Streams: all work is ordered after earlier work on `stream`, and later work on `stream` is
  * ordered after all of it.  For batches of >= 32 requests the call pipelines request sub-batches:
- * it forks part of the work onto internal high-priority streams (event fork/join, capture-safe)
- * and joins them back into `stream` before returning (SKV_SPLIT=n overrides the sub-batch count). */
+ * it forks part of the work onto the device's internal high-priority streams (event fork/join,
+ * capture-safe) and joins them back into `stream` before returning (SKV_SPLIT=n overrides the
+ * sub-batch count).  Calls from several host threads are safe (the fork/join enqueue is serialised
+ * per device); each concurrent call needs its own workspace. */
 SKV_API skv_status shadowkv_decode_step(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
                                 const uint16_t *q, const uint16_t *k_new, const uint16_t *v_new,
                                 int32_t step, uint16_t *out, int32_t *sel_ids, uint16_t *dbg_keys,

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libshadowkv.so")
 
 SKV_OK, SKV_EINVAL, SKV_EUNSUPPORTED, SKV_ECUDA, SKV_ESTATE = range(5)
 STATUS_NAMES = {0: "SKV_OK", 1: "SKV_EINVAL", 2: "SKV_EUNSUPPORTED", 3: "SKV_ECUDA", 4: "SKV_ESTATE"}
-EXPORTED = ["shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step", "shadowkv_decode_step_dev",
+EXPORTED = ["shadowkv_init", "shadowkv_score_plan", "shadowkv_rope_sincos", "shadowkv_workspace_bytes", "shadowkv_build_cache", "shadowkv_decode_step", "shadowkv_decode_step_dev",
             "shadowkv_last_error", "shadowkv_abi_version", "shadowkv_last_launch_count",
             "shadowkv_profile_begin", "shadowkv_profile_end", "shadowkv_trace_buffer",
             "shadowkv_factorize_workspace_bytes", "shadowkv_factorize"]
@@ -58,6 +58,12 @@ def load(path: str = LIB_PATH):
         raise ImportError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
     P = ctypes.POINTER
+    lib.shadowkv_init.restype = ctypes.c_int
+    lib.shadowkv_init.argtypes = [ctypes.c_int32]
+    lib.shadowkv_score_plan.restype = ctypes.c_int
+    lib.shadowkv_score_plan.argtypes = [P(SkvDims), ctypes.c_int32, P(ctypes.c_int32)]
+    lib.shadowkv_rope_sincos.restype = ctypes.c_int
+    lib.shadowkv_rope_sincos.argtypes = [P(SkvRope), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
     lib.shadowkv_workspace_bytes.restype = ctypes.c_size_t
     lib.shadowkv_workspace_bytes.argtypes = [P(SkvDims)]
     lib.shadowkv_build_cache.restype = ctypes.c_int
@@ -126,6 +132,37 @@ def layer_struct(A, B, landmarks, outlier_ids, K_out, V_out, K_win, V_win, V_hos
     return SkvLayer(_ptr(A), _ptr(B), _ptr(landmarks), _ptr(outlier_ids), _ptr(K_out), _ptr(V_out),
                     _ptr(K_win), _ptr(V_win), _ptr(V_host), _ptr(vc_values), _ptr(vc_dir), _ptr(vc_stats),
                     _ptr(A_gen))
+
+
+_INIT_DEVICES: set = set()
+
+
+def shadowkv_init(device: int | None = None):
+    """One-time per-device setup (kernel attributes, internal streams, tensor-map encoder)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    device = int(device)
+    if device not in _INIT_DEVICES:
+        _check(load().shadowkv_init(device))
+        _INIT_DEVICES.add(device)
+
+
+def ensure_init(device) -> None:
+    """shadowkv_init for a torch device ("cuda", "cuda:1", torch.device, index) if not done yet."""
+    d = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
+    if d.type == "cuda":
+        shadowkv_init(d.index if d.index is not None else torch.cuda.current_device())
+
+
+def shadowkv_score_plan(dims: SkvDims, n_sm: int):
+    """-> (grid, tiles_per_cta, heads_per_cta, ctas_per_head); raises ShadowKVError if unplannable."""
+    plan = (ctypes.c_int32 * 4)()
+    _check(load().shadowkv_score_plan(ctypes.byref(dims), int(n_sm), plan))
+    return tuple(int(x) for x in plan)
+
+
+def shadowkv_rope_sincos(rope: SkvRope, pos, n: int, sincos, stream=None):
+    _check(load().shadowkv_rope_sincos(ctypes.byref(rope), _ptr(pos), int(n), _ptr(sincos), _stream_ptr(stream)))
 
 
 def shadowkv_workspace_bytes(dims: SkvDims) -> int:

@@ -7,6 +7,8 @@
 #include <cstring>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "shadowkv.h"
 #include "kernels.h"
 
@@ -26,6 +28,39 @@ skv_status fail(skv_status st, const char* fmt, ...) {
   g_err = buf;
   return st;
 }
+
+// SKV_DEBUG_SYNC=1 (SURVEY §5 failure detection): after every enqueuing ABI call, synchronise the
+// stream and turn an asynchronous kernel fault into this call's SKV_ECUDA.  Skipped while the stream
+// is being captured into a CUDA graph (a sync there would invalidate the capture).
+skv_status debug_sync(void* stream, const char* call) {
+  static const bool on = [] { const char* v = getenv("SKV_DEBUG_SYNC"); return v && v[0] == '1'; }();
+  if (!on) return SKV_OK;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) cudaGetLastError();
+  if (cs != cudaStreamCaptureStatusNone) return SKV_OK;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SKV_ECUDA, "%s: kernel fault (SKV_DEBUG_SYNC): %s", call, cudaGetErrorString(e));
+  return SKV_OK;
+}
+
+// The device context shadowkv_init set up for the calling thread's current device.
+const skv::DevCtx* need_ctx() {
+  const skv::DevCtx* c = skv::current_ctx();
+  if (!c) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    cudaGetLastError();
+    fail(SKV_ESTATE, "shadowkv_init(%d) was not called for the current device", dev);
+  }
+  return c;
+}
+
+struct NvtxRange {             // an NVTX range around each ABI call (visible in nsys / ncu --nvtx)
+  explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -110,6 +145,14 @@ skv_status check_layer(const skv_layer* l, const skv::Dims& D, skv::Layer* Ly) {
   return SKV_OK;
 }
 
+// SKV_SERIALIZE=1 (SURVEY §5 race detection): no programmatic dependent launch between the decode
+// kernels, and every sparse-attention unit waits for its values before rebuilding its keys, i.e. the
+// overlapped schedule run serially.  Outputs must be bit-identical to the overlapped run (tested).
+int serial_mode() {
+  const char* v = getenv("SKV_SERIALIZE");
+  return v && v[0] == '1';
+}
+
 size_t ws_bytes(const skv::Dims& D) {
   return skv::build_ws_bytes(D, nullptr, nullptr);   // build scratch sits after every decode region
 }
@@ -147,6 +190,39 @@ skv::Profiler* g_prof = nullptr;
 }
 
 extern "C" {
+
+skv_status shadowkv_init(int32_t device) {
+  const char* what = "";
+  cudaError_t e = skv::init_device(device, &what);
+  if (e != cudaSuccess) { cudaGetLastError(); return fail(SKV_ECUDA, "shadowkv_init(%d): %s: %s", device, what, cudaGetErrorString(e)); }
+  g_err.clear();
+  return SKV_OK;
+}
+
+skv_status shadowkv_score_plan(const skv_dims* dims, int32_t n_sm, int32_t* plan) {
+  skv::Dims D;
+  skv_status st;
+  if ((st = check_dims(dims, &D)) != SKV_OK) return st;
+  if (n_sm < 1 || !plan) return fail(SKV_EINVAL, "n_sm must be >= 1 and plan non-NULL");
+  skv::ScorePlan p{};
+  const bool ok = skv::score_tc_plan(D, (D.n_c + skv::kSTile - 1) / skv::kSTile, n_sm, &p);
+  plan[0] = p.grid; plan[1] = p.tiles_per_cta; plan[2] = p.heads_per_cta; plan[3] = p.ctas_per_head;
+  if (!ok) return fail(SKV_EUNSUPPORTED, "no score grid for these dims: %d tiles / %d KV heads per CTA exceed the "
+                       "scorer's limits (a single request of this length needs more KV heads or a shorter context)",
+                       p.tiles_per_cta, p.heads_per_cta);
+  return SKV_OK;
+}
+
+skv_status shadowkv_rope_sincos(const skv_rope* rope, const int32_t* pos, int32_t n, float* sincos, void* stream) {
+  skv::Rope R;
+  skv_status st;
+  if ((st = check_rope(rope, 128, &R)) != SKV_OK) return st;
+  if (n < 0 || (n > 0 && (!pos || !sincos))) return fail(SKV_EINVAL, "n >= 0 and non-NULL pos / sincos required");
+  cudaError_t e = skv::launch_rope_probe(pos, n, R.inv_freq, R.rot / 2, sincos, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SKV_ECUDA, "rope probe: %s", cudaGetErrorString(e));
+  g_err.clear();
+  return SKV_OK;
+}
 
 skv_status shadowkv_profile_begin(int32_t capacity, int32_t kernel_mask) {
   if (g_prof) return fail(SKV_ESTATE, "profiling already active");
@@ -208,6 +284,7 @@ size_t shadowkv_workspace_bytes(const skv_dims* dims) {
 
 skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
                                 const uint16_t* K_rope, void* workspace, void* stream) {
+  NvtxRange nv("shadowkv_build_cache");
   skv::Dims D; skv::Rope R; skv::Layer Ly;
   skv_status st;
   if ((st = check_dims(dims, &D)) != SKV_OK) return st;
@@ -216,6 +293,7 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
   if (K_rope && !aligned16(K_rope)) return fail(SKV_EINVAL, "K_rope is not 16-byte aligned");
+  if (!need_ctx()) return SKV_ESTATE;
   // V_host must be page-locked and device-mapped at the same address (UVA), P:136 V^CPU
   cudaPointerAttributes attr;
   cudaError_t e = cudaPointerGetAttributes(&attr, Ly.V_host);
@@ -235,7 +313,7 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
   if (e != cudaSuccess) return fail(SKV_ECUDA, "build launch failed: %s", cudaGetErrorString(e));
   g_launches = launches;
   g_err.clear();
-  return SKV_OK;
+  return debug_sync(stream, "shadowkv_build_cache");
 }
 
 // Alg 1 "A, B <- SVD(K)": dims used are batch, n_kv_heads, head_dim, ctx_len, rank.
@@ -270,6 +348,7 @@ skv_status shadowkv_factorize(const skv_dims* dims, const uint16_t* K_pre, uint1
     return fail(SKV_EINVAL, "K_pre/A/B/sigma must be 16-byte aligned");
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
+  NvtxRange nv("shadowkv_factorize");
   skv::FactorizeWs ws;
   skv::factorize_ws_bytes(D, dims->rank, &ws, static_cast<char*>(workspace));
   int launches = 0;
@@ -281,13 +360,14 @@ skv_status shadowkv_factorize(const skv_dims* dims, const uint16_t* K_pre, uint1
                 cudaGetErrorString(r.err));
   g_launches = launches;
   g_err.clear();
-  return SKV_OK;
+  return debug_sync(stream, "shadowkv_factorize");
 }
 
 static skv_status decode_impl(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,
                               const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                               int32_t step, const int32_t* step_dev, uint16_t* out, int32_t* sel_ids,
                               uint16_t* dbg_keys, void* workspace, void* stream) {
+  NvtxRange nv(step_dev ? "shadowkv_decode_step_dev" : "shadowkv_decode_step");
   skv::Dims D; skv::Rope R; skv::Layer Ly;
   skv_status st;
   if ((st = check_dims(dims, &D)) != SKV_OK) return st;
@@ -315,13 +395,20 @@ static skv_status decode_impl(const skv_dims* dims, const skv_rope* rope, const 
     const int n = ns ? atoi(ns) : 1;
     D.trace_slot = n > 1 ? g_trace_calls++ % n : 0;
   }
+  const skv::DevCtx* ctx = need_ctx();
+  if (!ctx) return SKV_ESTATE;
+  D.serial = serial_mode();
   int launches = 0;
   cudaError_t e = skv::launch_decode(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, static_cast<char*>(workspace),
-                                     static_cast<cudaStream_t>(stream), &launches, g_prof);
+                                     static_cast<cudaStream_t>(stream), &launches, g_prof, *ctx);
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return fail(SKV_EUNSUPPORTED, "no tcgen05 score grid for these dims (see shadowkv_score_plan)");
+  }
   if (e != cudaSuccess) return fail(SKV_ECUDA, "decode launch failed: %s", cudaGetErrorString(e));
   g_launches = launches;
   g_err.clear();
-  return SKV_OK;
+  return debug_sync(stream, step_dev ? "shadowkv_decode_step_dev" : "shadowkv_decode_step");
 }
 
 skv_status shadowkv_decode_step(const skv_dims* dims, const skv_rope* rope, const skv_layer* layer,

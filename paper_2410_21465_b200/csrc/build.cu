@@ -124,12 +124,21 @@ size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base) {
   return off;
 }
 
+cudaError_t init_build_attrs() {
+  const int sm = (int)keytile_smem_bytes(256);          // the largest rank the ABI accepts
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_build_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  return cudaFuncSetAttribute(k_build_outliers_window, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+
+// Last kernel of every build: writes nothing.  decode's scorer is launched with PDL and reads the
+// layer state (landmarks, outlier ids) before its griddepcontrol.wait; PDL only orders the
+// preceding grid's writes after that wait, so the grid right before a decode must not write them.
+__global__ void k_build_done() {}
+
 cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* K_rope,
                          const BuildWs& ws, cudaStream_t st, int* launches) {
   const size_t sm = keytile_smem_bytes(D.r);
-  cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_build_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(k_build_outliers_window, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess) return e;
   dim3 g1((D.n_c + 15) / 16, D.hk, D.b);
   k_build_chunks<<<g1, kTileThreads, sm, st>>>(D, R, Ly, K_rope, ws.mincos, ws.negm);
   ++*launches;
@@ -143,6 +152,8 @@ cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const ui
     k_build_outliers_window<<<g3, kTileThreads, sm, st>>>(D, R, Ly, K_rope);
     ++*launches;
   }
+  k_build_done<<<1, 32, 0, st>>>();
+  ++*launches;
   return cudaGetLastError();
 }
 

@@ -35,7 +35,6 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
   return r;
 }
 
-// RoPE angle, R15: phi = fl32(fl32(t) * inv_freq) (no FMA contraction), accurate sincos.
 // RoPE angle phi = fl32(fl32(t) * inv_freq) (R15) and its sine / cosine.  Positions reach 2^20, so phi
 // reaches ~1e6 rad, where sincosf takes its slow (Payne-Hanek, local-memory) path.  phi is reduced
 // modulo 2 pi in fp64 instead (two-term 2 pi, |k| < 2^18: error < 1e-10 rad), then the fast path

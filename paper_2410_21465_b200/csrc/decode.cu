@@ -21,6 +21,8 @@
 // Kernels after the first are launched with programmatic dependent launch (PDL).
 #include <cstdlib>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "append.cuh"
 #include "kernels.h"
 #include "topk.cuh"
@@ -272,8 +274,7 @@ template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 2)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
          int score_total, int score_grid, int parts_per_cta, float* __restrict__ zws, int32_t* __restrict__ sel,
-         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int early_trigger,
-         int force_fb) {
+         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int force_fb) {
   TRACE_INIT;
   constexpr int NT = kSelThreads, NW = NT / 32;
   extern __shared__ __align__(16) float zdyn[];
@@ -297,7 +298,6 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * n + (size_t)lo * G;   // [n][G]
   int32_t* out = sel + bh * k;
   trace(1, 0);
-  if (early_trigger) pdl_trigger();                     // sparse-attn CTAs may start their prologue
   for (int i = tid; i < 256; i += NT) hist[i] = 0;
   if (tid == 0) { ccnt = 0; info[0] = 255; info[1] = 0; }   // B = 255 unless bins 0..254 reach k
   cluster_arrive_relaxed();                             // #0: this CTA has started (waited on before the
@@ -373,7 +373,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   trace(1, 3);
   cluster_sync_all();                                                   // #1 histograms published
   trace(1, 4);
-  if (!early_trigger) pdl_trigger();                    // sparse CTAs launch and poll their slots
+  pdl_trigger();                                        // sparse CTAs launch and poll their slots
   if (tid < 256) {
     int g = 0;
 #pragma unroll
@@ -812,6 +812,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     if (early_next) pdl_trigger();                       // next layer's score may become resident
     trace(2, 2);
     __syncthreads();
+    if (D.serial) mbar_wait(&barV, 0);                   // SKV_SERIALIZE: values first, then the rebuild
     mbar_wait(&barAB, 0);
     trace(2, 3);
     // ---- K~ = A_rows . B_h on the tensor cores (bf16 x bf16 -> fp32, mma.sync m16n8k16): a 64 x 128 x r
@@ -1004,6 +1005,23 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   trace(2, 8);
 }
 
+// Diagnostic (shadowkv_rope_sincos): the sine / cosine of the RoPE angle phi = fl32(fl32(t) *
+// inv_freq[i]) exactly as the decode kernels compute it, for n positions x rot/2 frequencies.
+__global__ void k_rope_probe(const int32_t* __restrict__ pos, int n, const float* __restrict__ inv_freq, int nf,
+                             float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * nf) return;
+  float s, c;
+  rope_sincos(pos[i / nf], inv_freq[i % nf], &s, &c);
+  out[2 * (size_t)i] = s;
+  out[2 * (size_t)i + 1] = c;
+}
+cudaError_t launch_rope_probe(const int32_t* pos, int n, const float* inv_freq, int nf, float* out, cudaStream_t st) {
+  const int total = n * nf;
+  if (total > 0) k_rope_probe<<<(total + 255) / 256, 256, 0, st>>>(pos, n, inv_freq, nf, out);
+  return cudaGetLastError();
+}
+
 // =============================================================================================
 // host side
 // =============================================================================================
@@ -1044,14 +1062,14 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
 }
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr; cfg.numAttrs = 1;
+  cfg.attrs = attr; cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -1065,86 +1083,91 @@ __global__ void k_relay() { pdl_trigger(); }
 // tuning switches (process environment, read once); the test hooks SKV_NO_TC and
 // SKV_SELECT_FALLBACK are read per call because tests toggle them inside one process
 struct Tuning {
-  int early_sel, early_next, relay, merge_late;
+  int early_next, relay, merge_late;
 };
 static const Tuning& tuning() {
   static const Tuning t = [] {
     auto is = [](const char* name, char c) { const char* v = getenv(name); return v && v[0] == c; };
-    return Tuning{is("SKV_EARLY_TRIGGER", '1') ? 1 : 0, is("SKV_SPARSE_TRIGGER", '0') ? 0 : 1,
-                  is("SKV_NO_RELAY", '1') ? 0 : 1, is("SKV_MERGE_TRIGGER", 'l') ? 1 : 0};
+    return Tuning{is("SKV_SPARSE_TRIGGER", '0') ? 0 : 1, is("SKV_NO_RELAY", '1') ? 0 : 1,
+                  is("SKV_MERGE_TRIGGER", 'l') ? 1 : 0};
   }();
   return t;
 }
 
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+// kernel attributes of every decode instantiation, set once per device by shadowkv_init
+template <int G>
+static cudaError_t set_decode_attrs_g() {
+  cudaError_t e;
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  // CUDA-core scorer (test hook SKV_NO_TC): its outlier bitmap grows with n_c, so allow the device maximum
+  if ((e = cudaFuncGetAttributes(&fa, k_score<G>))) return e;
+  if ((e = cudaFuncSetAttribute(k_score<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes))) return e;
+  if ((e = cudaFuncSetAttribute(k_select<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelectSmemMax))) return e;
+  if ((e = cudaFuncSetAttribute(k_sparse_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)attn_smem_layout(256, G).bytes))) return e;
+  return cudaSuccess;
+}
+cudaError_t init_decode_attrs() {
+  cudaError_t e;
+  if ((e = set_decode_attrs_g<1>()) || (e = set_decode_attrs_g<2>()) || (e = set_decode_attrs_g<4>()) ||
+      (e = set_decode_attrs_g<8>()) || (e = set_decode_attrs_g<16>())) return e;
+  return cudaSuccess;
 }
 
 template <int G>
 static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                                    const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                                    int32_t* sel_ids, uint16_t* dbg_keys, const DecodeWs& ws,
-                                   cudaStream_t st, int* launches, Profiler* prof, cudaEvent_t ev_sel) {
+                                   cudaStream_t st, int* launches, Profiler* prof, cudaEvent_t ev_sel,
+                                   const DevCtx& ctx) {
   const float scale = (float)(1.0 / 11.313708498984761);    // 1/sqrt(d), d = 128 (R6)
-  static size_t score_attr = 0;
-  static bool attrs_set = false;
   const AttnSmem lay = attn_smem_layout(D.r, G);
-  const size_t score_smem = (size_t)kSStages * kSTile * kHeadDim * 2 + 2 * G * kSTile * 4 +
-                            (size_t)((D.n_c + 31) / 32) * 4;
   cudaError_t e;
-  if (score_smem > score_attr) {
-    if ((e = cudaFuncSetAttribute(k_score<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem))) return e;
-    score_attr = score_smem;
-  }
-  if (!attrs_set) {
-    if ((e = cudaFuncSetAttribute(k_select<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSelectSmemMax))) return e;
-    if ((e = cudaFuncSetAttribute(k_sparse_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)attn_smem_layout(256, G).bytes))) return e;
-    attrs_set = true;
-  }
   const int tph = ws.n_sblk;
   const int total_tiles = D.b * D.hk * tph;
-  int grid_s = total_tiles < 2 * num_sms() ? total_tiles : 2 * num_sms();
-  while (grid_s > 1 && (long long)tph * grid_s / total_tiles + 2 > kSegMax) --grid_s;   // select's slots
-  // a1: tcgen05 score (TMA + TMEM); CUDA-core fallback when tensor maps are unavailable
-  int score_grid = score_tc_grid(D, tph, num_sms());
-  int parts_per_cta = 2;                                // k_score_tc: one softmax partial per epilogue group
-  const char* nt = getenv("SKV_NO_TC");                 // test hook: force the CUDA-core score
-  e = (nt && nt[0] == '1') ? cudaErrorNotSupported
-                           : launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
-                                                v_new, Ly.K_win, Ly.V_win, step, num_sms(), st);
-  if (prof && e == cudaSuccess) profile_mark(prof, kScore, false, st);
-  if (e == cudaErrorNotSupported || e == cudaErrorInvalidValue) {
-    cudaGetLastError();
+  // a1: the tcgen05 scorer (TMA + TMEM).  The CUDA-core k_score is a test hook only (SKV_NO_TC=1):
+  // a failing tensor-map encode or an unplannable grid is an error, not a silent second backend.
+  int score_grid, parts_per_cta;
+  const char* nt = getenv("SKV_NO_TC");
+  if (prof) profile_mark(prof, kScore, false, st);
+  nvtxRangePushA("skv::score");
+  if (nt && nt[0] == '1') {
+    int grid_s = total_tiles < 2 * ctx.n_sm ? total_tiles : 2 * ctx.n_sm;
+    while (grid_s > 1 && (long long)tph * grid_s / total_tiles + 2 > kSegMax) --grid_s;   // select's slots
+    const size_t score_smem = (size_t)kSStages * kSTile * kHeadDim * 2 + 2 * G * kSTile * 4 +
+                              (size_t)((D.n_c + 31) / 32) * 4;
     score_grid = grid_s;
     parts_per_cta = 1;
-    if (prof) profile_mark(prof, kScore, false, st);
     k_score<G><<<grid_s, 256, score_smem, st>>>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
                                                 v_new, Ly.K_win, Ly.V_win, step);
     e = cudaGetLastError();
+  } else {
+    ScorePlan pl;
+    if (!score_tc_plan(D, tph, ctx.n_sm, &pl)) return cudaErrorNotSupported;
+    score_grid = pl.grid;
+    parts_per_cta = 2;                                  // k_score_tc: one softmax partial per epilogue group
+    e = launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new, v_new, Ly.K_win,
+                           Ly.V_win, step, ctx, st);
   }
+  nvtxRangePop();
   if (e) return e;
   if (prof) { profile_mark(prof, kScore, true, st); profile_mark(prof, kSelect, false, st); }
   {
-    const int early_sel = tuning().early_sel;            // 1 = PDL trigger at kernel start
     const char* fb = getenv("SKV_SELECT_FALLBACK");       // test hook: 1 / 2 force the radix fallback
     const int force_fb = fb ? atoi(fb) : 0;               // before / after the definite chunks publish
+    nvtxRangePushA("skv::select");
     const bool zsm = z_fits_smem(D, G);
     const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
-    if (zsm) e = launch_pdl(k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
+    if (zsm) e = launch_pdl(!D.serial, k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                             (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, parts_per_cta, ws.z,
-                            ws.sel, ws.selrest, ws.flags, sel_ids, early_sel, force_fb);
-    else e = launch_pdl(k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
+                            ws.sel, ws.selrest, ws.flags, sel_ids, force_fb);
+    else e = launch_pdl(!D.serial, k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                         (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, parts_per_cta, ws.z,
-                        ws.sel, ws.selrest, ws.flags, sel_ids, early_sel, force_fb);
+                        ws.sel, ws.selrest, ws.flags, sel_ids, force_fb);
+    nvtxRangePop();
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
     if (ev_sel && (e = cudaEventRecord(ev_sel, st))) return e;   // sub-batch pipelining: next chain may start
@@ -1160,19 +1183,25 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score
   // grid then launches only when this grid drains)
   const int early_next = tuning().early_next;
-  if ((e = launch_pdl(k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
+  nvtxRangePushA("skv::sparse_attn");
+  e = launch_pdl(!D.serial, k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
                       ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
-                      n_sel_u, n_out_u, n_win_u, n_gen_u, n_split, scale, dbg_keys, early_next))) return e;
+                      n_sel_u, n_out_u, n_win_u, n_gen_u, n_split, scale, dbg_keys, early_next);
+  nvtxRangePop();
+  if (e) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
   if (tuning().relay) {                                  // SKV_NO_RELAY=1 omits the relay grid
-    if ((e = launch_pdl(k_relay, dim3(1), dim3(32), 0, st))) return e;
+    if ((e = launch_pdl(!D.serial, k_relay, dim3(1), dim3(32), 0, st))) return e;
     *launches += 1;
   }
   const int merge_late = tuning().merge_late;            // SKV_MERGE_TRIGGER=late: after the loads
   if (prof) profile_mark(prof, kCombine, false, st);
-  if ((e = launch_pdl(k_merge<G>, dim3(D.b * D.hq), dim3(kHeadDim), (size_t)n_split * (sizeof(float2) + sizeof(float)), st, D,
+  nvtxRangePushA("skv::merge");
+  e = launch_pdl(!D.serial, k_merge<G>, dim3(D.b * D.hq), dim3(kHeadDim), (size_t)n_split * (sizeof(float2) + sizeof(float)), st, D,
                       (const float*)ws.o_part, (const float2*)ws.ml_part, n_split, ws.sel, ws.flags, out,
-                      merge_late, Ly.vc_stats))) return e;
+                      merge_late, Ly.vc_stats);
+  nvtxRangePop();
+  if (e) return e;
   if (prof) profile_mark(prof, kCombine, true, st);
   *launches += 4;
   return cudaGetLastError();
@@ -1181,13 +1210,13 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
 static cudaError_t launch_decode_one(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                                      const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                                      int32_t* sel_ids, uint16_t* dbg_keys, const DecodeWs& ws, cudaStream_t st,
-                                     int* launches, Profiler* prof, cudaEvent_t ev_sel) {
+                                     int* launches, Profiler* prof, cudaEvent_t ev_sel, const DevCtx& ctx) {
   switch (D.g) {
-    case 1: return launch_decode_g<1>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel);
-    case 2: return launch_decode_g<2>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel);
-    case 4: return launch_decode_g<4>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel);
-    case 8: return launch_decode_g<8>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel);
-    case 16: return launch_decode_g<16>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel);
+    case 1: return launch_decode_g<1>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel, ctx);
+    case 2: return launch_decode_g<2>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel, ctx);
+    case 4: return launch_decode_g<4>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel, ctx);
+    case 8: return launch_decode_g<8>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel, ctx);
+    case 16: return launch_decode_g<16>(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, ev_sel, ctx);
   }
   return cudaErrorInvalidValue;
 }
@@ -1200,7 +1229,6 @@ static cudaError_t launch_decode_one(const Dims& D, const Rope& R, const Layer& 
 // The caller's stream joins every chain before returning.  Each chain has its own workspace region.
 // Measured gain is small (c3, 64 requests, 4 chains: +2 %; c5, 12 requests: none): the chains'
 // sparse grids hold the SMs, so a later chain's scoring only gets slots as earlier CTAs retire.
-constexpr int kMaxSplit = 8;
 static int split_count(const Dims& D) {
   static const int env = [] { const char* v = getenv("SKV_SPLIT"); return v ? atoi(v) : 0; }();
   const int n = env > 0 ? env : (D.b >= 32 ? 4 : 1);   // measured: +2 % at c3 (64), none at c5 (12)
@@ -1227,28 +1255,21 @@ size_t decode_ws_total_bytes(const Dims& D) {
 cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                           const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                           int32_t* sel_ids, uint16_t* dbg_keys, char* ws_base, cudaStream_t st,
-                          int* launches, Profiler* prof) {
+                          int* launches, Profiler* prof, const DevCtx& ctx) {
   const int nd = split_count(D);
   const int n = prof ? 1 : nd;
   if (n == 1) {
     DecodeWs ws;
     decode_ws_bytes(D, &ws, ws_base + (nd > 1 ? split_ws_bytes(D, nd, nullptr) : 0));
-    return launch_decode_one(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, nullptr);
+    return launch_decode_one(D, R, Ly, q, k_new, v_new, step, out, sel_ids, dbg_keys, ws, st, launches, prof, nullptr,
+                             ctx);
   }
-  static cudaStream_t side[kMaxSplit];
-  static cudaEvent_t ev_sel[kMaxSplit], ev_done[kMaxSplit];
-  static bool init = false;
+  // the chains' streams and events belong to the device context (created by shadowkv_init)
+  const cudaStream_t* side = ctx.side;
+  const cudaEvent_t* ev_sel = ctx.ev_sel;
+  const cudaEvent_t* ev_done = ctx.ev_done;
+  std::lock_guard<std::mutex> lk(chain_mutex(ctx.device));   // one call's fork/join at a time per device
   cudaError_t e;
-  if (!init) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);          // hi = greatest priority (numerically lowest)
-    for (int i = 0; i < kMaxSplit; ++i) {
-      if ((e = cudaStreamCreateWithPriority(&side[i], cudaStreamNonBlocking, hi))) return e;
-      if ((e = cudaEventCreateWithFlags(&ev_sel[i], cudaEventDisableTiming))) return e;
-      if ((e = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming))) return e;
-    }
-    init = true;
-  }
   size_t offs[kMaxSplit];
   split_ws_bytes(D, n, offs);
   const size_t s = D.s, hk = D.hk, hq = D.hq, d = kHeadDim;
@@ -1280,7 +1301,7 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
                           v_new + (size_t)r0 * hk * D.sq * d,
                           step, out + (size_t)r0 * hq * d, sel_ids ? sel_ids + (size_t)r0 * hk * D.k : nullptr,
                           dbg_keys ? dbg_keys + (size_t)r0 * hk * D.k * kChunk * d : nullptr, ws, si, launches,
-                          nullptr, i + 1 < n ? ev_sel[i] : nullptr);
+                          nullptr, i + 1 < n ? ev_sel[i] : nullptr, ctx);
     if (e) return e;
   }
   for (int i = 1; i < n; ++i) {                          // the caller's stream joins every chain

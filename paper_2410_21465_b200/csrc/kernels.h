@@ -4,6 +4,8 @@
 #include <stdint.h>
 #include <stddef.h>
 
+#include <mutex>
+
 namespace skv {
 
 struct Dims {          // validated, derived sizes
@@ -18,6 +20,7 @@ struct Dims {          // validated, derived sizes
   // low-rank generated keys (NEXT-4; nullable = plain window): the layer's B and its A_gen rows
   const uint16_t* lr_B;
   uint16_t* lr_A;      // [b][wcap][r]: row g = generated token g (decode step index)
+  int serial;          // SKV_SERIALIZE: no PDL overlap, values before rebuild (bit-identical check)
 };
 #ifdef __CUDACC__
 // per-request sizes of a ragged batch (R8 applied to each request's own length)
@@ -100,13 +103,39 @@ void profile_mark(Profiler* p, int kernel, bool end, cudaStream_t st);
 cudaError_t set_trace_buffer(void* dev_ptr);      // decode.cu: nullptr disables
 cudaError_t set_trace_buffer_tc(void* dev_ptr);   // score_tc.cu (kernel slot 0)
 
-// score_tc.cu: tcgen05 landmark scoring (a1); cudaErrorNotSupported if tensor maps are unavailable
-int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm);
+// ---- per-device runtime context (shadowkv_init): everything a decode / build call would otherwise
+// create or configure on first use -- kernel smem attributes, the sub-batch side streams and events,
+// the SM count, the driver's tensor-map encoder -- is set up once per device, under a lock, so the
+// hot path never allocates and concurrent calls (different streams / devices) share nothing mutable.
+constexpr int kMaxSplit = 8;                      // request sub-batch chains (decode.cu)
+constexpr int kMaxDevices = 64;
+struct DevCtx {
+  int device = -1;
+  int n_sm = 0;
+  cudaStream_t side[kMaxSplit] = {};
+  cudaEvent_t ev_sel[kMaxSplit] = {}, ev_done[kMaxSplit] = {};
+  void* encode_tiled = nullptr;                   // cuTensorMapEncodeTiled (driver entry point)
+};
+// the calling thread's current device's context, or nullptr if shadowkv_init was not called for it
+const DevCtx* current_ctx();
+cudaError_t init_device(int device, const char** what);   // idempotent; thread-safe
+cudaError_t init_decode_attrs();                  // decode.cu: kernel attributes (current device)
+cudaError_t init_build_attrs();                   // build.cu
+cudaError_t init_score_tc_attrs();                // score_tc.cu
+std::mutex& chain_mutex(int device);              // serialises sub-batch chain enqueues per device
+
+// score_tc.cu: tcgen05 landmark scoring (a1).  The plan must satisfy the kernel's static limits (tiles
+// and KV heads per CTA, partial slots per head); score_tc_plan returns false (and the decode call
+// SKV_EUNSUPPORTED) when no grid does, e.g. a single request of several million tokens.
+struct ScorePlan {
+  int grid, tiles_per_cta, heads_per_cta, ctas_per_head;
+};
+bool score_tc_plan(const Dims& D, int tiles_per_head, int n_sm, ScorePlan* plan);
 template <int G>
 cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
                             float* logits, float2* part, int tiles_per_head, float scale,
                             const uint16_t* k_new, const uint16_t* v_new, uint16_t* K_win, uint16_t* V_win,
-                            int step, int n_sm, cudaStream_t st);
+                            int step, const DevCtx& ctx, cudaStream_t st);
 
 // each returns cudaGetLastError() after its launches and adds to *launches
 cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* K_rope,
@@ -114,8 +143,9 @@ cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const ui
 cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                           const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                           int32_t* sel_ids, uint16_t* dbg_keys, char* ws_base, cudaStream_t st,
-                          int* launches, Profiler* prof);
+                          int* launches, Profiler* prof, const DevCtx& ctx);
 size_t decode_ws_total_bytes(const Dims& D);   // every sub-batch split's workspace fits
+cudaError_t launch_rope_probe(const int32_t* pos, int n, const float* inv_freq, int nf, float* out, cudaStream_t st);
 
 // factorize.cu: Alg 1 "A, B <- SVD(K)" through the D x D Gram matrix (NEXT-2)
 constexpr size_t kFactorizeBlasWs = (size_t)32 << 20;   // cuBLAS workspace carved from ours

@@ -6,7 +6,7 @@
 //
 // CUDA-core fp32 version (v1): A rows and B_h staged in shared memory, 256 threads, each
 // thread accumulates 8 tokens x 8 dims; RoPE applied in place on the fp32 tile
-// (angle fl32(fl32(t) * inv_freq), accurate sincosf -- R15).  Result: fp32 [128][128] in smem.
+// (angle fl32(fl32(t) * inv_freq), reduced mod 2 pi in fp64, hardware sincos on |r| <= pi -- R15, rope_sincos).  Result: fp32 [128][128] in smem.
 #pragma once
 #include "common.cuh"
 

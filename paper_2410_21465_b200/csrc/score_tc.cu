@@ -29,7 +29,7 @@ namespace {
 constexpr int kTcStages = 6;
 constexpr int kTcAcc = 8;                 // TMEM accumulator buffers (16 fp32 columns each)
 constexpr int kTcMaxHeads = 4;            // KV heads a CTA's contiguous tile range may touch
-constexpr int kTcMaxTiles = 64;           // tiles per CTA (bitmap size); host sizes the grid accordingly
+constexpr int kTcMaxTiles = 256;          // tiles per CTA (outlier bitmap size, 4 KB); checked by the plan
 constexpr int kTcThreads = 352;         // 2 x 4 epilogue warps, 1 TMA producer, 2 MMA issuers
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __restrict__ oids,
            const uint16_t* __restrict__ q, float* __restrict__ logits, float2* __restrict__ part,
            int tiles_per_head, float scale, const uint16_t* __restrict__ k_new,
-           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step, int early_trigger) {
+           const uint16_t* __restrict__ v_new, uint16_t* K_win, uint16_t* V_win, int step) {
   static_assert(G <= 16, "N = 16 covers the GQA group");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -133,7 +133,6 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   uint64_t* const trace_buf = g_trace_tc ? g_trace_tc + (size_t)D.trace_slot * kTraceSlot : nullptr;
   const uint64_t pol = l2_evict_first_policy();
   trace_tc(trace_buf, 0);
-  if (early_trigger) pdl_trigger();
   // the producer thread initialises the barriers and puts the first kTcStages tiles in flight
   // before anything else, so HBM streaming starts at kernel entry
   if (tid == 4 * 32 && ntile > 0) {
@@ -324,7 +323,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   }
   __syncthreads();
   trace_tc(trace_buf, 1);
-  if (!early_trigger) pdl_trigger();
+  pdl_trigger();
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" :: "r"(tmem));
@@ -334,42 +333,45 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
 // ---------------------------------------------------------------------------------------------
 // host: tensor map over the landmark matrix viewed as [b*h_kv*n_c rows][128] bf16
 // ---------------------------------------------------------------------------------------------
-static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    cudaGetLastError();
-  }
-  return fn;
-}
-
 size_t score_tc_smem_bytes() { return 1024 + (size_t)kTcStages * kTileBytes + (size_t)kTcMaxHeads * kBBytes; }
 
-int score_tc_grid(const Dims& D, int tiles_per_head, int n_sm) {
-  const int total = D.b * D.hk * tiles_per_head;
-  int grid = total < n_sm ? total : n_sm;
+bool score_tc_plan(const Dims& D, int tiles_per_head, int n_sm, ScorePlan* plan) {
+  const long long total = (long long)D.b * D.hk * tiles_per_head;
+  if (total <= 0 || total * (long long)(2 * n_sm) >= (1ll << 31)) return false;   // seg_first: 32-bit
+  int grid = total < n_sm ? (int)total : n_sm;
   // each CTA's contiguous tile range must touch at most kTcMaxHeads KV heads and kTcMaxTiles tiles
-  while (grid < total && ((total + grid - 1) / grid > (kTcMaxHeads - 1) * tiles_per_head ||
+  while (grid < total && ((total + grid - 1) / grid > (long long)(kTcMaxHeads - 1) * tiles_per_head ||
                           (total + grid - 1) / grid > kTcMaxTiles))
-    grid = grid * 2 < total ? grid * 2 : total;
-  // at most kSegMax score CTAs may cover one KV head (k_select's partial slots)
-  while (grid > 1 && 2 * ((long long)tiles_per_head * grid / total + 2) > kSegMax) --grid;   // 2 per CTA
-  return grid;
+    grid = grid * 2 < total ? grid * 2 : (int)total;
+  // at most kSegMax partial slots (two per CTA) per KV head: k_select reads them in one pass
+  while (grid > 1 && 2 * ((long long)tiles_per_head * grid / total + 2) > kSegMax) --grid;
+  // the second loop may lower the grid below the first loop's bounds again: re-check both limits
+  const int tpc = (int)((total + grid - 1) / grid);
+  const int heads = (tpc + tiles_per_head - 1) / tiles_per_head + 1;     // a range may straddle one more
+  if (plan) *plan = ScorePlan{grid, tpc, heads, (int)((long long)tiles_per_head * grid / total + 2)};
+  return tpc <= kTcMaxTiles && heads <= kTcMaxHeads;
+}
+
+cudaError_t init_score_tc_attrs() {
+  cudaError_t e = cudaSuccess;
+  auto set = [&](const void* f) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_tc_smem_bytes());
+  };
+  set((const void*)k_score_tc<1>); set((const void*)k_score_tc<2>); set((const void*)k_score_tc<4>);
+  set((const void*)k_score_tc<8>); set((const void*)k_score_tc<16>);
+  return e;
 }
 
 template <int G>
 cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oids, const uint16_t* q,
                             float* logits, float2* part, int tiles_per_head, float scale,
                             const uint16_t* k_new, const uint16_t* v_new, uint16_t* K_win, uint16_t* V_win,
-                            int step, int n_sm, cudaStream_t st) {
-  auto enc = get_encode();
+                            int step, const DevCtx& ctx, cudaStream_t st) {
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
   if (!enc) return cudaErrorNotSupported;
+  ScorePlan pl;
+  if (!score_tc_plan(D, tiles_per_head, ctx.n_sm, &pl)) return cudaErrorNotSupported;
   CUtensorMap map;
   const cuuint64_t gdim[2] = {(cuuint64_t)kHeadDim, (cuuint64_t)D.b * D.hk * D.n_c};
   const cuuint64_t gstride[1] = {(cuuint64_t)kHeadDim * 2};
@@ -379,31 +381,21 @@ cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oid
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  cudaError_t e;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(k_score_tc<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)score_tc_smem_bytes()))) return e;
-    attr = true;
-  }
-  const int grid = score_tc_grid(D, tiles_per_head, n_sm);
-  const char* et = getenv("SKV_EARLY_TRIGGER");            // tuning hook: 1 = PDL trigger at kernel start
-  const int early = (et && et[0] == '1') ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(kTcThreads); cfg.dynamicSmemBytes = score_tc_smem_bytes();
+  cfg.gridDim = dim3(pl.grid); cfg.blockDim = dim3(kTcThreads); cfg.dynamicSmemBytes = score_tc_smem_bytes();
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;     // prologue overlaps the prior kernel
   at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at; cfg.numAttrs = 1;
+  cfg.attrs = at; cfg.numAttrs = D.serial ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, k_score_tc<G>, map, D, oids, q, logits, part, tiles_per_head, scale, k_new, v_new,
-                            K_win, V_win, step, early);
+                            K_win, V_win, step);
 }
 
 #define SKV_INST(G)                                                                                       \
   template cudaError_t launch_score_tc<G>(const Dims&, const uint16_t*, const int32_t*, const uint16_t*,  \
                                           float*, float2*, int, float, const uint16_t*, const uint16_t*,  \
-                                          uint16_t*, uint16_t*, int, int, cudaStream_t);
+                                          uint16_t*, uint16_t*, int, const DevCtx&, cudaStream_t);
 SKV_INST(1)
 SKV_INST(2)
 SKV_INST(4)

@@ -60,6 +60,7 @@ class Shape:
 
 
 def alloc_workspace(shape: Shape, device="cuda") -> torch.Tensor:
+    bd.ensure_init(device)
     n = bd.shadowkv_workspace_bytes(shape.dims())
     return torch.zeros(n + 256, dtype=torch.uint8, device=device)     # ABI: zero-filled before first use
 
@@ -75,6 +76,7 @@ class LayerState:
     def __init__(self, shape: Shape, device="cuda", V_host: torch.Tensor | None = None,
                  value_cache: bool = False, lowrank_gen: bool = False):
         self.shape = S = shape
+        bd.ensure_init(device)                          # shadowkv_init for this device (once)
         b, hk, d = S.batch, S.n_kv_heads, S.head_dim
         self.lens_host = self.lens_dev = None
         if S.ctx_lens is not None:                      # ragged batch: host + device length arrays
@@ -145,6 +147,7 @@ def factorize(K_pre: torch.Tensor, rank: int, stream=None):
     """Alg 1 "A, B <- SVD(K)" on the GPU through shadowkv_factorize.
     K_pre: device bf16 [b][h_kv][s][d] -> (A bf16 [b][s][r], B bf16 [b][h_kv][r][d], sigma fp32 [b][r])."""
     b, hk, s, d = K_pre.shape
+    bd.ensure_init(K_pre.device)
     dims = bd.dims_struct(b, hk, hk, d, s, rank, 8, 0, 1, 0, 1)
     n = bd.shadowkv_factorize_workspace_bytes(dims)
     ws = torch.empty(n + 256, dtype=torch.uint8, device=K_pre.device)

@@ -27,7 +27,7 @@ def test_header_declares_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert bd.shadowkv_abi_version() == 5
+    assert bd.shadowkv_abi_version() == 6
 
 
 def _dims(**kw):
@@ -184,3 +184,49 @@ def test_shape_window_capacity_for_ragged_and_multi_query():
     wide = Shape.from_config(cfg.replace(ctx_len=4100), steps=1, ctx_lens=[4096, 2064, 1040])
     assert wide.window_cap == 20 + 1
     assert bd.shadowkv_workspace_bytes(wide.dims()) > 0
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_score_plan_every_config(lib, name):
+    """The tcgen05 scorer has a launch plan for every BASELINE config on a 148-SM B200, within its static
+    limits (<= 256 tiles and <= 4 KV heads per CTA, <= 64 partial slots per KV head)."""
+    shp = Shape.from_config(synth.CONFIGS[name])
+    grid, tpc, heads, cph = bd.shadowkv_score_plan(shp.dims(), 148)
+    tph = -(-shp.n_c // 128)
+    assert 1 <= grid <= 2 * 148 and tpc <= 256 and heads <= 4 and 2 * cph <= 64
+    assert grid * tpc >= shp.batch * shp.n_kv_heads * tph          # every tile is covered
+
+
+@pytest.mark.parametrize("ctx", [1 << 21, 1 << 22, 7 << 20])
+def test_score_plan_long_single_request(lib, ctx):
+    """one request of 2M / 4M / 7M tokens (8 KV heads) used to overflow the scorer's
+    64-tile outlier bitmap once the partial-slot limit lowered the grid; the plan re-checks both limits."""
+    d = _dims(ctx_len=ctx, budget=ctx // 512, n_outlier=48, window_cap=64)
+    grid, tpc, heads, cph = bd.shadowkv_score_plan(d, 148)
+    assert tpc <= 256 and heads <= 4 and 2 * cph <= 64
+    assert grid * tpc >= 8 * -(-((ctx - 16) // 8) // 128)
+
+
+def test_score_plan_rejects_what_no_grid_fits(lib):
+    """Beyond the kernel's limits the plan (and decode_step) says SKV_EUNSUPPORTED instead of
+    launching a kernel that would overrun its shared-memory bitmap."""
+    d = _dims(ctx_len=(1 << 24) - 65536 - 8, budget=1024, n_outlier=48, window_cap=64)
+    assert lib.shadowkv_score_plan(ctypes.byref(d), 148, (ctypes.c_int32 * 4)()) == bd.SKV_EUNSUPPORTED
+    assert "tiles" in lib.shadowkv_last_error().decode()
+    ok = _dims()
+    assert lib.shadowkv_score_plan(ctypes.byref(ok), 0, (ctypes.c_int32 * 4)()) == bd.SKV_EINVAL
+
+
+def test_decode_needs_init_before_any_cuda(lib):
+    """Valid arguments on a device shadowkv_init was not called for: SKV_ESTATE, nothing enqueued
+    (here: no GPU at all, so no device is ever initialised)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    d = _dims(window_cap=64)
+    rope = bd.SkvRope(128, 0, 16)
+    layer = bd.SkvLayer(*([16] * 9 + [None] * 4))
+    st = lib.shadowkv_decode_step(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(layer), 16, 16, 16, 0, 16, None,
+                                  None, 256, None)
+    assert st == bd.SKV_ESTATE and "shadowkv_init" in lib.shadowkv_last_error().decode()
+    assert lib.shadowkv_init(0) == bd.SKV_ECUDA

@@ -80,3 +80,37 @@ def test_tokens_per_rank_sum_to_the_batch():
         assert abs(sum(shares) - batch) < 1e-12
         if batch < world:
             assert all(abs(x - 1.0 / world) < 1e-12 for x in shares) or hk % world
+
+
+def _bench_dry(*extra):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", *extra], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout                       # rank 0 alone prints
+    return lines[0]
+
+
+def test_bench_gpus_2_self_launches_two_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run, 127.0.0.1);
+    c3 defaults to strong scaling (64 requests split 64/n): each rank owns 32 requests and the
+    ranks' token shares sum to the job's batch."""
+    out = _bench_dry("--gpus", "2", "--config", "c3")
+    assert out["n_gpus"] == 2 and out["scaling"] == "strong"
+    assert sorted(tuple(p["requests"]) for p in out["ranks"]) == [(0, 32), (32, 64)]
+    assert out["tokens_per_step"] == 64
+
+
+def test_bench_gpus_2_c2_weak_and_kv_head_split():
+    """c2 defaults to weak scaling (one 128K request per GPU); --scaling strong splits its 8 KV heads."""
+    out = _bench_dry("--gpus", "2", "--config", "c2")
+    assert out["n_gpus"] == 2 and out["scaling"] == "weak" and out["tokens_per_step"] == 2
+    out = _bench_dry("--gpus", "2", "--config", "c2", "--scaling", "strong")
+    assert sorted(tuple(p["kv_heads"]) for p in out["ranks"]) == [(0, 4), (4, 8)]
+    assert all(p["mode"] == "kv_head" for p in out["ranks"]) and abs(out["tokens_per_step"] - 1.0) < 1e-12
