@@ -229,7 +229,7 @@ def softmax_attention(q, keys, values):
 
 
 def decode_step(state: BuildState, A, B, V, q, k_new, v_new, step, k, inv_freq, rotary_dim,
-                interleaved, c, store=bf16_round):
+                interleaved, c, store=bf16_round, sel=None):
     """One decode step of Alg 2 + sparse attention (R17, R18).
 
     q [b][h_q][d] (s_q = 1) or [b][h_q][s_q][d] (Alg 2's Q, NEXT-3; k_new, v_new then
@@ -238,10 +238,16 @@ def decode_step(state: BuildState, A, B, V, q, k_new, v_new, step, k, inv_freq, 
     state is NOT modified; returns (out [b][h_q][d] or [b][h_q][s_q][d], sel [b][h_kv][k],
     z [b][h_kv][n_c], rebuilt keys [b][h_kv][k*c][d] (unrounded), new_state with the window
     slots written).
+
+    sel (optional, [b][h_kv][k] chunk ids): attend these chunks instead of ArgTopK's I (z is still
+    computed and returned).  Test hook for R23: where the GPU's set differs from the oracle's only by
+    a tie swap within 1e-5 (R1), keys and outputs are compared with the oracle evaluated on the GPU's
+    set, which is the same algorithm after step "I <- ArgTopK".
     """
     if np.ndim(q) == 4:
         return _decode_step_multi(state, A, B, V, q, k_new, v_new, step, k, inv_freq, rotary_dim,
-                                  interleaved, c, store)
+                                  interleaved, c, store, sel)
+    given = sel
     A = np.asarray(A, np.float64); B = np.asarray(B, np.float64); V = np.asarray(V, np.float64)
     q = np.asarray(q, np.float64); k_new = np.asarray(k_new, np.float64)
     v_new = np.asarray(v_new, np.float64)
@@ -266,7 +272,7 @@ def decode_step(state: BuildState, A, B, V, q, k_new, v_new, step, k, inv_freq, 
             qg = q[bi, h * g:(h + 1) * g]
             logits = landmark_scores(qg, st.landmarks[bi, h], d)
             z = normalise_group_max(logits, mask)
-            ids = arg_topk(z, k)
+            ids = arg_topk(z, k) if given is None else np.sort(np.asarray(given[bi][h], np.int64))
             tok = (ids[:, None] * c + np.arange(c)[None, :]).reshape(-1)
             kt = rebuild_keys(A[bi], B[bi, h], tok, inv_freq, rotary_dim, interleaved)
             vt = V[bi, h, tok]                           # Gather(V^CPU, I)
@@ -286,8 +292,9 @@ def decode_step(state: BuildState, A, B, V, q, k_new, v_new, step, k, inv_freq, 
 
 
 def _decode_step_multi(state, A, B, V, q, k_new, v_new, step, k, inv_freq, rotary_dim, interleaved, c,
-                       store):
+                       store, sel=None):
     """decode_step for s_q >= 1 query tokens (Alg 2 with Q in R^{b x h_q x s_q x d})."""
+    given = sel
     A = np.asarray(A, np.float64); B = np.asarray(B, np.float64); V = np.asarray(V, np.float64)
     q = np.asarray(q, np.float64); k_new = np.asarray(k_new, np.float64)
     v_new = np.asarray(v_new, np.float64)
@@ -311,7 +318,7 @@ def _decode_step_multi(state, A, B, V, q, k_new, v_new, step, k, inv_freq, rotar
             qg = q[bi, h * g:(h + 1) * g]                               # [g][s_q][d]
             logits = np.stack([landmark_scores(qg[:, i], st.landmarks[bi, h], d) for i in range(sq)], axis=1)
             z = normalise_sum_group_max(logits, mask)
-            ids = arg_topk(z, k)
+            ids = arg_topk(z, k) if given is None else np.sort(np.asarray(given[bi][h], np.int64))
             tok = (ids[:, None] * c + np.arange(c)[None, :]).reshape(-1)
             kt = rebuild_keys(A[bi], B[bi, h], tok, inv_freq, rotary_dim, interleaved)
             vt = V[bi, h, tok]

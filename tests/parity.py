@@ -116,26 +116,46 @@ class Problem:
         torch.cuda.synchronize()
         return f64(out), sel.cpu().numpy(), f64(dbg)
 
-    def oracle_decode(self, ost, step, si, store=O.bf16_round):
+    def oracle_decode(self, ost, step, si, store=O.bf16_round, sel=None):
         c = self.cfg
         return O.decode_step(ost, self.A64, self.B64, self.V64, f64(si["q"]), f64(si["k_new"]), f64(si["v_new"]),
-                             step, c.budget, self.inv, self.rot, self.il, c.chunk, store=store)
+                             step, c.budget, self.inv, self.rot, self.il, c.chunk, store=store, sel=sel)
+
+    def check(self, ost, step, si, gpu):
+        """GPU decode result `gpu` = (out, sel, keys) of this step vs the oracle from state `ost` (R1, R23);
+        returns (exact head count, the oracle's next state)."""
+        gout, gsel, gkeys = gpu
+        oout, osel, oz, okeys, nst = self.oracle_decode(ost, step, si)
+        exact = check_decode(self.cfg, gout, gsel, gkeys, oout, osel, oz, okeys,
+                             rerun=lambda sel: self.oracle_decode(ost, step, si, sel=sel))
+        return exact, nst
 
 
-def check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys, require_exact_frac=0.9):
-    """Selection valid per head (R1); keys and outputs compared on heads whose sets are identical."""
+def check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys, rerun=None):
+    """Every head: the GPU's selection is the oracle's or a valid tie swap of it (R1); the rebuilt keys
+    (per-row relative L2 <= 1e-2) and the outputs (max-abs <= 2e-2) are compared on EVERY head (R23):
+    against the oracle's own results where the sets are equal, else against the oracle evaluated on the
+    GPU's set -- rerun(gsel) -> oracle.decode_step(..., sel=gsel)'s tuple, from the same prior state.
+    Returns the number of heads whose selection equals the oracle's exactly."""
     b, hk, g = cfg.batch, cfg.n_kv_heads, cfg.n_q_heads // cfg.n_kv_heads
     exact = 0
     for bi in range(b):
         for h in range(hk):
             assert selection_valid(gsel[bi, h], oz[bi, h], cfg.budget), \
                 f"invalid selection b={bi} h={h}: gpu {gsel[bi, h][:8]}.. oracle {osel[bi, h][:8]}.."
-            if np.array_equal(gsel[bi, h], osel[bi, h]):
-                exact += 1
-                kg, ko = gkeys[bi, h], okeys[bi, h]
-                rel = np.linalg.norm(kg - ko, axis=1) / np.maximum(np.linalg.norm(ko, axis=1), 1e-6)
-                assert rel.max() <= KEY_REL_TOL, f"rebuilt keys rel err {rel.max():.3g} (b={bi} h={h})"
-                err = np.abs(gout[bi, h * g:(h + 1) * g] - oout[bi, h * g:(h + 1) * g]).max()
-                assert err <= OUT_TOL, f"output max-abs {err:.3g} > {OUT_TOL} (b={bi} h={h})"
-    assert exact >= require_exact_frac * b * hk, f"only {exact}/{b * hk} heads with identical selection"
+            exact += int(np.array_equal(gsel[bi, h], osel[bi, h]))
+    if exact < b * hk:
+        assert rerun is not None, f"{b * hk - exact} tie-swapped head(s): pass rerun= to compare them"
+        r = rerun(gsel)
+        oout_g, okeys_g = r[0], r[3]
+    for bi in range(b):
+        for h in range(hk):
+            same = np.array_equal(gsel[bi, h], osel[bi, h])
+            ko = okeys[bi, h] if same else okeys_g[bi, h]
+            oo = oout if same else oout_g
+            kg = gkeys[bi, h]
+            rel = np.linalg.norm(kg - ko, axis=1) / np.maximum(np.linalg.norm(ko, axis=1), 1e-6)
+            assert rel.max() <= KEY_REL_TOL, f"rebuilt keys rel err {rel.max():.3g} (b={bi} h={h}, same set {same})"
+            err = np.abs(gout[bi, h * g:(h + 1) * g] - oo[bi, h * g:(h + 1) * g]).max()
+            assert err <= OUT_TOL, f"output max-abs {err:.3g} > {OUT_TOL} (b={bi} h={h}, same set {same})"
     return exact

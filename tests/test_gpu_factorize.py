@@ -70,7 +70,7 @@ def test_factorize_then_decode_matches_oracle():
     """Prefill fully on the GPU: factorize -> build_cache (keys = RoPE(A.B)) -> decode_step, against the
     oracle running build + decode on the same (GPU-produced) factors."""
     from paper_2410_21465_b200 import factorize
-    from tests.parity import Problem, check_decode, outliers_valid
+    from tests.parity import Problem, outliers_valid
     cfg = synth.CONFIGS["c1"].replace(ctx_len=2048, budget=16)
     P = Problem(cfg, seed=4, steps=2)
     K = torch.einsum("btr,bhrd->bhtd", P.inputs["A"].float(), P.inputs["B"].float()).to(torch.bfloat16)
@@ -85,5 +85,4 @@ def test_factorize_then_decode_matches_oracle():
     P.load_state_from_oracle(ost)
     si = P.step_inputs(0)
     gout, gsel, gkeys = P.gpu_decode(0, si)
-    oout, osel, oz, okeys, _ = P.oracle_decode(ost, 0, si)
-    check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
+    P.check(ost, 0, si, (gout, gsel, gkeys))

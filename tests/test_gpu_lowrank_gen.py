@@ -12,7 +12,7 @@ import torch
 
 import synth
 from oracle import shadowkv_oracle as O
-from tests.parity import Problem, assert_bf16_close, check_decode, f64
+from tests.parity import Problem, assert_bf16_close, f64
 
 pytestmark = pytest.mark.gpu
 
@@ -40,6 +40,5 @@ def test_lowrank_generated_keys_parity(name, q_len):
         a, keys = O.lowrank_generated_keys(kp4, P.B64, s + step + np.arange(q_len), P.inv, P.rot, P.il)
         si_o = dict(si)
         si_o["k_new"] = torch.from_numpy(keys if kp.ndim == 4 else keys[:, :, 0])
-        oout, osel, oz, okeys, ost = P.oracle_decode(ost, step, si_o)
-        check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
+        _, ost = P.check(ost, step, si_o, (gout, gsel, gkeys))
         assert_bf16_close(f64(P.st.A_gen[:, step:step + q_len]), a, abs_slack=1e-6, what="A_gen rows")

@@ -96,11 +96,14 @@ def test_ragged_batch_parity(name, q_len, value_cache):
             assert torch.equal(out, out2) and torch.equal(sel, sel2), "value cache changed a ragged result"
         for b in sample:
             sb = lens[b]
-            oo, os_, oz, ok, ost[b] = O.decode_step(ost[b], A64[b:b + 1, :sb], B64[b:b + 1], V64[b:b + 1, :, :sb],
-                                                    f64(si["q"][b:b + 1]), f64(si["k_new"][b:b + 1]),
-                                                    f64(si["v_new"][b:b + 1]), step, k, inv, rot, il, c)
+            run = lambda st0, sel_=None, b=b, sb=sb: O.decode_step(
+                st0, A64[b:b + 1, :sb], B64[b:b + 1], V64[b:b + 1, :, :sb], f64(si["q"][b:b + 1]),
+                f64(si["k_new"][b:b + 1]), f64(si["v_new"][b:b + 1]), step, k, inv, rot, il, c, sel=sel_)
+            st_prev = ost[b]
+            oo, os_, oz, ok, ost[b] = run(st_prev)
             assert sel[b].max().item() < ost[b].n_c, "selected a chunk past the request's own grid"
-            check_decode(one, f64(out[b:b + 1]), sel[b:b + 1].cpu().numpy(), f64(dbg[b:b + 1]), oo, os_, oz, ok)
+            check_decode(one, f64(out[b:b + 1]), sel[b:b + 1].cpu().numpy(), f64(dbg[b:b + 1]), oo, os_, oz, ok,
+                         rerun=lambda s_, st_prev=st_prev, run=run: run(st_prev, s_))
     if value_cache:
         assert int(st.cache_stats()[..., 3].sum()) > 0, "drifting queries produced no cache hits"
 

@@ -13,7 +13,7 @@ import torch
 
 import synth
 from oracle import shadowkv_oracle as O
-from tests.parity import Problem, check_decode
+from tests.parity import Problem
 
 pytestmark = pytest.mark.gpu
 
@@ -62,8 +62,7 @@ def test_value_cache_parity_and_hits(name):
         gout, gsel, gkeys = P.gpu_decode(t, si)
         rout, rsel, _ = P.gpu_decode(t, si, st=ref)
         assert np.array_equal(gout, rout) and np.array_equal(gsel, rsel), f"cache changed the result at step {t}"
-        oout, osel, oz, okeys, ost = P.oracle_decode(ost, t, si)
-        check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys)
+        _, ost = P.check(ost, t, si, (gout, gsel, gkeys))
         stats = P.st.cache_stats().numpy()
         assert (stats[..., 0] == t + 1).all()                      # one generation per decode step
         for bi in range(b):

@@ -401,3 +401,41 @@ def test_multi_query_full_coverage_equals_causal_dense_attention(sq):
             keys = np.concatenate([keys_ctx, np.stack(gk, axis=1)], axis=1)
             vals = np.concatenate([V[0], np.stack(gv, axis=1)], axis=1)
             np.testing.assert_allclose(out[0, :, i], O.dense_attention(q[0, :, i], keys, vals), atol=1e-12)
+
+
+@pytest.mark.parametrize("sq", [1, 2])
+def test_given_selection_equals_dense_attention_over_that_set(sq):
+    """decode_step(sel=J) (the R23 test hook: oracle evaluated on the GPU's set) attends exactly the
+    outlier tokens, the tokens of the chunks in J (any order given) and the window: equal to dense
+    attention over that explicit token subset with independently rebuilt keys (self-check mode)."""
+    s, hk, g, d, c, o, w = 203, 2, 2, 16, 8, 3, 5
+    A, B, V, inv, rot, rng = _small_problem(21, s=s, hk=hk, g=g, d=d, w=w)
+    n_c, w_eff = O.partition(s, c, w)
+    st = O.build(A, B, V, inv, rot, False, c, o, w, window_cap=w_eff + 4, store=O.identity_store)
+    keys_ctx = np.stack([_rope_complex(A[0] @ B[0, h], np.arange(s), inv, rot, False) for h in range(hk)])
+    k = 5
+    J = np.stack([rng.permutation([j for j in range(n_c) if j not in set(st.outlier_ids[0, h])])[:k]
+                  for h in range(hk)])[None]
+    q = rng.normal(size=(1, hk * g, sq, d)) * 2 if sq > 1 else rng.normal(size=(1, hk * g, d)) * 2
+    kn = rng.normal(size=(1, hk, sq, d)) if sq > 1 else rng.normal(size=(1, hk, d))
+    vn = rng.normal(size=(1, hk, sq, d)) if sq > 1 else rng.normal(size=(1, hk, d))
+    out, sel, z, kt, _ = O.decode_step(st, A, B, V, q, kn, vn, 0, k, inv, rot, False, c, store=O.identity_store,
+                                       sel=J)
+    for h in range(hk):
+        assert list(sel[0, h]) == sorted(J[0, h])
+        toks = sorted({t for j in list(J[0, h]) + list(st.outlier_ids[0, h]) for t in range(j * c, j * c + c)} |
+                      set(range(n_c * c, s)))
+        for i in range(sq):
+            kn_i = kn[0, h, i] if sq > 1 else kn[0, h]
+            vn_i = vn[0, h, i] if sq > 1 else vn[0, h]
+            gk = np.stack([kn[0, h, t] for t in range(i + 1)]) if sq > 1 else kn_i[None]
+            gv = np.stack([vn[0, h, t] for t in range(i + 1)]) if sq > 1 else vn_i[None]
+            keys = np.concatenate([keys_ctx[h, toks], gk])
+            vals = np.concatenate([V[0, h, toks], gv])
+            for j in range(g):
+                qq = q[0, h * g + j, i] if sq > 1 else q[0, h * g + j]
+                got = out[0, h * g + j, i] if sq > 1 else out[0, h * g + j]
+                np.testing.assert_allclose(got, O.dense_attention(qq[None], keys[None], vals[None])[0], atol=1e-12)
+        # the rebuilt keys are reported in the ascending order of the given set
+        tk = [t for j in sorted(J[0, h]) for t in range(j * c, j * c + c)]
+        np.testing.assert_allclose(kt[0, h], keys_ctx[h, tk], atol=1e-12)
