@@ -149,7 +149,6 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
   if (tid == 0)
     for (int it = 0; it < kSStages - 1; ++it) issue(it);
   float qr[G][8];
-  float seg_m[2] = {-INFINITY, -INFINITY}, seg_s[2] = {0.f, 0.f};   // running partial of heads warp, warp+8
   int cur_bh = -1;
   for (int it = 0; t_begin + it < t_end; ++it) {
     const int t = t_begin + it;
@@ -196,7 +195,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
       const int r = idx / G, hq = idx - r * G;
       if (r < rows) lb[idx] = Pb[hq * kSTile + r];
     }
-    for (int hq = warp; hq < G; hq += 8) {           // tile softmax partial merged into the segment's
+    for (int hq = warp; hq < G; hq += 8) {           // the tile's softmax partial (per-tile: batch invariant)
       float x[kSTile / 32];
       float m = -INFINITY;
 #pragma unroll
@@ -208,14 +207,7 @@ k_score(Dims D, const uint16_t* __restrict__ L, const int32_t* __restrict__ oids
         for (int u = 0; u < kSTile / 32; ++u) sm += expf(x[u] - m);
       }
       sm = warp_sum(sm);
-      lse_merge(seg_m[hq >> 3], seg_s[hq >> 3], m, sm);
-      const bool last_of_seg = (it + 1 == t_end - t_begin) || ((t + 1) / tiles_per_head != bh);
-      if (last_of_seg) {
-        if (lane == 0)
-          part[((size_t)b * D.hq + (size_t)h * G + hq) * kSegMax +
-               ((int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x))] = make_float2(seg_m[hq >> 3], seg_s[hq >> 3]);
-        seg_m[hq >> 3] = -INFINITY; seg_s[hq >> 3] = 0.f;
-      }
+      if (lane == 0) part[((size_t)b * D.hq + (size_t)h * G + hq) * tiles_per_head + tile] = make_float2(m, sm);
     }
   }
   trace(0, 1);
@@ -273,7 +265,7 @@ __device__ __forceinline__ float group_z(const float* lg, const float* lse) {
 template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 2)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
-         int score_total, int score_grid, int parts_per_cta, float* __restrict__ zws, int32_t* __restrict__ sel,
+         float* __restrict__ zws, int32_t* __restrict__ sel,
          int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int force_fb) {
   TRACE_INIT;
   constexpr int NT = kSelThreads, NW = NT / 32;
@@ -305,19 +297,20 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   trace(1, 1);
   int* fl = flags + bh * 4;
   if (crank == 0 && tid == 0) st_release_gpu(&fl[0], 1);  // score (incl. a7 window append) complete
-  // ---- lse_hq from the score CTAs' per-segment partials: max-reduce, one exp per lane, sum-reduce
-  //      (short dependent chains; fixed order, deterministic)
+  // ---- lse_hq from the score kernel's per-tile partials: max-reduce, exp-sum-reduce, each in a fixed
+  //      order (lane-strided, then the warp tree): deterministic and independent of the score grid
   if (warp < G) {
-    const int nseg = parts_per_cta * seg_count((int)bh, tiles_per_head, score_total, score_grid);
     if (warp == 0) trace(1, 13);
-    const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * kSegMax;
-    float2 v0 = lane < nseg ? ph[lane] : make_float2(-INFINITY, 0.f);
-    float2 v1 = lane + 32 < nseg ? ph[lane + 32] : make_float2(-INFINITY, 0.f);   // nseg <= kSegMax = 64
-    const float m = warp_max(fmaxf(v0.x, v1.x));
+    const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * tiles_per_head;
+    float m = -INFINITY;
+    for (int i = lane; i < tiles_per_head; i += 32) m = fmaxf(m, __ldcg(&ph[i].x));
+    m = warp_max(m);
     if (warp == 0) trace(1, 14);
     float e = 0.f;
-    if (v0.x > -INFINITY) e += v0.y * expf(v0.x - m);
-    if (v1.x > -INFINITY) e += v1.y * expf(v1.x - m);
+    for (int i = lane; i < tiles_per_head; i += 32) {
+      const float2 v = __ldcg(&ph[i]);
+      if (v.x > -INFINITY) e += v.y * expf(v.x - m);
+    }
     const float sm = warp_sum(e);
     if (lane == 0) { lse[warp] = m + logf(sm); hm[warp] = m; }
     if (warp == 0) trace(1, 15);
@@ -1039,7 +1032,7 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
   const int n_split = n_sel_u + n_out_u + n_win_max;
   const size_t BHq = (size_t)D.b * D.hq, BHk = (size_t)D.b * D.hk;
   char* p_log = carve(BHq * D.n_c * 4);
-  char* p_part = carve(BHq * kSegMax * 8);          // per-(score CTA, head) softmax partials
+  char* p_part = carve(BHq * tph * 8);              // per-(tile, query row) softmax partials
   char* p_z = carve(BHk * D.n_c * 4);                // select fallback / large-n_c slices
   char* p_sel = carve(BHk * D.k * 4);                // definite selections (and the radix fallback)
   char* p_rest = carve(BHk * D.k * 4);               // threshold-bucket selections
@@ -1130,25 +1123,19 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   const int total_tiles = D.b * D.hk * tph;
   // a1: the tcgen05 scorer (TMA + TMEM).  The CUDA-core k_score is a test hook only (SKV_NO_TC=1):
   // a failing tensor-map encode or an unplannable grid is an error, not a silent second backend.
-  int score_grid, parts_per_cta;
   const char* nt = getenv("SKV_NO_TC");
   if (prof) profile_mark(prof, kScore, false, st);
   nvtxRangePushA("skv::score");
   if (nt && nt[0] == '1') {
-    int grid_s = total_tiles < 2 * ctx.n_sm ? total_tiles : 2 * ctx.n_sm;
-    while (grid_s > 1 && (long long)tph * grid_s / total_tiles + 2 > kSegMax) --grid_s;   // select's slots
+    const int grid_s = total_tiles < 2 * ctx.n_sm ? total_tiles : 2 * ctx.n_sm;
     const size_t score_smem = (size_t)kSStages * kSTile * kHeadDim * 2 + 2 * G * kSTile * 4 +
                               (size_t)((D.n_c + 31) / 32) * 4;
-    score_grid = grid_s;
-    parts_per_cta = 1;
     k_score<G><<<grid_s, 256, score_smem, st>>>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new,
                                                 v_new, Ly.K_win, Ly.V_win, step);
     e = cudaGetLastError();
   } else {
     ScorePlan pl;
     if (!score_tc_plan(D, tph, ctx.n_sm, &pl)) return cudaErrorNotSupported;
-    score_grid = pl.grid;
-    parts_per_cta = 2;                                  // k_score_tc: one softmax partial per epilogue group
     e = launch_score_tc<G>(D, Ly.L, Ly.outlier_ids, q, ws.logits, ws.part, tph, scale, k_new, v_new, Ly.K_win,
                            Ly.V_win, step, ctx, st);
   }
@@ -1162,10 +1149,10 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     const bool zsm = z_fits_smem(D, G);
     const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
     if (zsm) e = launch_pdl(!D.serial, k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
-                            (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, parts_per_cta, ws.z,
+                            (const float*)ws.logits, (const float2*)ws.part, tph, ws.z,
                             ws.sel, ws.selrest, ws.flags, sel_ids, force_fb);
     else e = launch_pdl(!D.serial, k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
-                        (const float*)ws.logits, (const float2*)ws.part, tph, total_tiles, score_grid, parts_per_cta, ws.z,
+                        (const float*)ws.logits, (const float2*)ws.part, tph, ws.z,
                         ws.sel, ws.selrest, ws.flags, sel_ids, force_fb);
     nvtxRangePop();
     if (e) return e;

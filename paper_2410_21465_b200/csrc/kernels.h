@@ -62,7 +62,7 @@ struct DecodeWs {
   int32_t* selrest;  // [b][hk][k] radix-fallback scratch (top-k, ascending)
   float* logits;     // [b][hk][n_c][G]: landmark-major, the G rows of a landmark contiguous (one vector
                      // store in the score epilogue, one vector load per landmark in k_select)
-  float2* part;      // [b][hq][kSegMax] per-(score CTA, head) softmax partials (max, sumexp)
+  float2* part;      // [b][hq][tiles_per_head] per-tile softmax partials (max, sumexp) of each query row
   float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
   int32_t* sel;      // [b][hk][k] published selection, unordered, chunk id + 1 (0 = not yet); re-zeroed
   float* o_part;     // [b][hq][n_split][d]
@@ -77,18 +77,6 @@ constexpr size_t kSelectSmemMax = 160 * 1024;     // per-CTA z slice + its logit
 constexpr int kSelCL = 8;                         // select: CTAs per (request, KV head) cluster
 constexpr int kSelThreads = 512;
 constexpr int kSelCandLocal = 1024;               // threshold-bucket candidates per CTA
-constexpr int kSegMax = 64;                       // score partial slots per (b, q head)
-
-// first score CTA whose contiguous tile range [floor(c*T/g), floor((c+1)*T/g)) covers head bh
-// (32-bit: the host keeps total * grid < 2^31; 64-bit division is a slow software routine on the GPU)
-__host__ __device__ inline int seg_first(int bh, int tiles_per_head, int total, int grid) {
-  return (int)(((unsigned)(bh * tiles_per_head) * (unsigned)grid + (unsigned)grid - 1u) / (unsigned)total);
-}
-__host__ __device__ inline int seg_count(int bh, int tiles_per_head, int total, int grid) {
-  const unsigned last_tile = (unsigned)((bh + 1) * tiles_per_head - 1);
-  return (int)((last_tile * (unsigned)grid + (unsigned)grid - 1u) / (unsigned)total) -
-         seg_first(bh, tiles_per_head, total, grid) + 1;
-}
 
 // header: per-(b,h) merge counter + 4 selection flags {def_ready, n_def, rest_ready, n_rest}
 inline size_t ws_header_bytes(const Dims& D) { return ((size_t)D.b * D.hk * 5 * 4 + 255) & ~(size_t)255; }

@@ -29,7 +29,7 @@ namespace {
 constexpr int kTcStages = 6;
 constexpr int kTcAcc = 8;                 // TMEM accumulator buffers (16 fp32 columns each)
 constexpr int kTcMaxHeads = 4;            // KV heads a CTA's contiguous tile range may touch
-constexpr int kTcMaxTiles = 256;          // tiles per CTA (outlier bitmap size, 4 KB); checked by the plan
+constexpr int kTcMaxTiles = 64;           // tiles per CTA (outlier bitmap size); the plan never exceeds it
 constexpr int kTcThreads = 352;         // 2 x 4 epilogue warps, 1 TMA producer, 2 MMA issuers
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
@@ -123,7 +123,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], acc_full[kTcAcc], acc_empty[kTcAcc];
   __shared__ uint32_t tmem_base;
   __shared__ uint32_t obits[kTcMaxTiles * (kSTile / 32)];
-  __shared__ float2 wpart[2][4][16];
+  __shared__ float2 wpart[2][2][4][16];                        // [group][tile parity][warp][row]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = D.b * D.hk * tiles_per_head;
   const int t_begin = (int)((long long)blockIdx.x * total / gridDim.x);
@@ -240,55 +240,30 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     }
   } else {
     // ---------------- epilogue: two groups of 4 warps (0-3 and 7-10) on alternate tiles ----------------
-    // Warp w reads TMEM lane quadrant w % 4.  A single warp per sub-partition was latency / issue bound
-    // (~1000 cycles per tile at G = 16); two groups halve the per-tile work of each.  Each group keeps
-    // per-thread online softmax partials over its rows of each KV head and flushes one partial per
-    // (CTA, KV head, group) at slot 2 * (CTA index - seg_first()) + group (k_select reads 2 per CTA);
-    // a group flushes an empty partial for every head of the CTA's range it saw no tile of, so the
-    // slot set stays complete and both groups pass the same named barriers.
-    // Branch-free online update in the log2 domain, one independent chain per head (ILP); a finite
-    // floor stands in for -inf so that fully masked rows never produce inf - inf.
+    // Warp w reads TMEM lane quadrant w % 4 (32 landmark rows).  Per tile and query row it writes the
+    // logits and ONE softmax partial (max, sum exp) of the tile's 128 landmarks: the four warps' partials
+    // meet in smem behind one named barrier of the group and warp quad 0 merges them in a fixed order.
+    // A KV head's lse is then the fixed-order merge of its tiles' partials (k_select), independent of
+    // how tiles are spread over CTAs: a (request, KV head)'s result does not depend on the batch it
+    // runs in (batch / head sharding is bit-exact).  Log2 domain; a finite floor stands in for -inf so
+    // fully masked rows never produce inf - inf.
     constexpr float kFloor = -1e30f, kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
     const int grp = warp >= 7 ? 1 : 0, quad = warp & 3;
-    float m_run[G], s_run[G];
-#pragma unroll
-    for (int hq = 0; hq < G; ++hq) { m_run[hq] = kFloor; s_run[hq] = 0.f; }
-    auto flush = [&](int bh) {
-      const int b = bh / D.hk, h = bh - b * D.hk;
-      const int slot = 2 * ((int)blockIdx.x - seg_first(bh, tiles_per_head, total, (int)gridDim.x)) + grp;
-#pragma unroll
-      for (int hq = 0; hq < G; ++hq) {
-        const float m2 = warp_max(m_run[hq]);
-        const float sm = warp_sum(s_run[hq] * exp2f(m_run[hq] - m2));
-        if (lane == 0) wpart[grp][quad][hq] = m2 > kFloor ? make_float2(m2 * kLn2, sm) : make_float2(-INFINITY, 0.f);
-        m_run[hq] = kFloor; s_run[hq] = 0.f;
-      }
-      if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");   // the group's 4 warps
-      else asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (quad == 0 && lane < G) {
-        float m = -INFINITY, sm = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) lse_merge(m, sm, wpart[grp][w][lane].x, wpart[grp][w][lane].y);
-        part[((size_t)b * D.hq + (size_t)h * G + lane) * kSegMax + slot] = make_float2(m, sm);
-      }
-      if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
-      else asm volatile("bar.sync 2, 128;" ::: "memory");
-    };
-    const int bh_last = (t_end - 1) / tiles_per_head;
     int bh = t_begin / tiles_per_head, tile = t_begin - bh * tiles_per_head;   // advanced incrementally
     if (grp == 1 && ntile > 1) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
-    int cur_bh = t_begin / tiles_per_head;
-    float* lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
-    int ncb = req_nc(D, bh / D.hk);                       // ragged batch: chunks past it are masked
+    int cur_bh = -1;
+    float* lrow = nullptr;
+    float2* prow = nullptr;
+    int ncb = 0;
     const int r = 32 * quad + lane;
     for (int i = grp; i < ntile; i += 2) {
-      const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1;
+      const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1, par = (i >> 1) & 1;
       if (bh != cur_bh) {
-        flush(cur_bh);                                    // (and empty partials for heads skipped)
-        for (int e = cur_bh + 1; e < bh; ++e) flush(e);
         cur_bh = bh;
-        lrow = logits + (size_t)((bh / D.hk) * D.hq + (bh % D.hk) * G) * D.n_c;
-        ncb = req_nc(D, bh / D.hk);
+        const int b = bh / D.hk, h = bh - b * D.hk;
+        lrow = logits + (size_t)(b * D.hq + h * G) * D.n_c;
+        prow = part + (size_t)(b * D.hq + h * G) * tiles_per_head;
+        ncb = req_nc(D, b);                               // ragged batch: chunks past it are masked
       }
       mbar_wait(&acc_full[buf], aph);
       tc_fence_after();
@@ -298,28 +273,36 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
       const int j = tile * kSTile + r;
-      const bool out = ((obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u) || j >= ncb;
+      const bool out = ((obits[(i * kSTile + r) >> 5] >> (r & 31)) & 1u) || j >= ncb || j >= D.n_c;
       if (warp == 0 && lane == 0 && i < 4) trace_tc_any(trace_buf, 8 + i);   // epilogue got tile i
-      if (j < D.n_c) {
-        float xs[G];
+      float xs[G];
 #pragma unroll
-        for (int hq = 0; hq < G; ++hq) xs[hq] = out ? -INFINITY : v[hq] * scale;
-        store_row<G>(lrow + (size_t)j * G, xs);             // landmark-major logits [n_c][G]
+      for (int hq = 0; hq < G; ++hq) xs[hq] = out ? -INFINITY : v[hq] * scale;
+      if (j < D.n_c) store_row<G>(lrow + (size_t)j * G, xs);   // landmark-major logits [n_c][G]
 #pragma unroll
-        for (int hq = 0; hq < G; ++hq) {
-          const float x = xs[hq];
-          const float x2 = out ? kFloor : x * kLog2e;
-          const float mn = fmaxf(m_run[hq], x2);
-          s_run[hq] = fmaf(s_run[hq], exp2f(m_run[hq] - mn), out ? 0.f : exp2f(x2 - mn));
-          m_run[hq] = mn;
+      for (int hq = 0; hq < G; ++hq) {
+        const float x2 = out ? kFloor : xs[hq] * kLog2e;
+        const float m2 = warp_max(x2);
+        const float sm = warp_sum(out ? 0.f : exp2f(x2 - m2));
+        if (lane == 0) wpart[grp][par][quad][hq] = make_float2(m2, sm);
+      }
+      if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");   // the group's 4 warps
+      else asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (quad == 0 && lane < G) {                        // fixed-order merge of the 4 warps (log2 domain)
+        float m = kFloor;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) m = fmaxf(m, wpart[grp][par][w][lane].x);
+        float sm = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float2 pw = wpart[grp][par][w][lane];
+          sm += pw.y * exp2f(pw.x - m);
         }
+        prow[(size_t)lane * tiles_per_head + tile] = m > kFloor ? make_float2(m * kLn2, sm) : make_float2(-INFINITY, 0.f);
       }
       for (int st2 = 0; st2 < 2; ++st2) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
     }
     if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 13);     // epilogue loop done
-    flush(cur_bh);
-    for (int e = cur_bh + 1; e <= bh_last; ++e) flush(e);          // heads this group saw no tile of
-    if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 14);     // partials flushed
   }
   __syncthreads();
   trace_tc(trace_buf, 1);
@@ -337,18 +320,15 @@ size_t score_tc_smem_bytes() { return 1024 + (size_t)kTcStages * kTileBytes + (s
 
 bool score_tc_plan(const Dims& D, int tiles_per_head, int n_sm, ScorePlan* plan) {
   const long long total = (long long)D.b * D.hk * tiles_per_head;
-  if (total <= 0 || total * (long long)(2 * n_sm) >= (1ll << 31)) return false;   // seg_first: 32-bit
+  if (total <= 0 || total >= (1ll << 31)) return false;
   int grid = total < n_sm ? (int)total : n_sm;
   // each CTA's contiguous tile range must touch at most kTcMaxHeads KV heads and kTcMaxTiles tiles
   while (grid < total && ((total + grid - 1) / grid > (long long)(kTcMaxHeads - 1) * tiles_per_head ||
                           (total + grid - 1) / grid > kTcMaxTiles))
     grid = grid * 2 < total ? grid * 2 : (int)total;
-  // at most kSegMax partial slots (two per CTA) per KV head: k_select reads them in one pass
-  while (grid > 1 && 2 * ((long long)tiles_per_head * grid / total + 2) > kSegMax) --grid;
-  // the second loop may lower the grid below the first loop's bounds again: re-check both limits
   const int tpc = (int)((total + grid - 1) / grid);
   const int heads = (tpc + tiles_per_head - 1) / tiles_per_head + 1;     // a range may straddle one more
-  if (plan) *plan = ScorePlan{grid, tpc, heads, (int)((long long)tiles_per_head * grid / total + 2)};
+  if (plan) *plan = ScorePlan{grid, tpc, heads, (int)((tiles_per_head * (long long)grid + total - 1) / total)};
   return tpc <= kTcMaxTiles && heads <= kTcMaxHeads;
 }
 

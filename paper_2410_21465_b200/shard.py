@@ -87,3 +87,31 @@ def sum_over_ranks(value: float, device=None) -> float:
 def job_tokens_per_s(tokens_this_rank: float, step_s_this_rank: float, device=None) -> float:
     """Whole-job decode tokens/s: all ranks' tokens per step / max-over-ranks step time."""
     return sum_over_ranks(tokens_this_rank, device) / max_over_ranks(step_s_this_rank, device)
+
+
+def shard_state(state, p: Plan):
+    """The shard of one layer's state a rank owns under plan p, as VIEWS of `state`'s tensors (no copy):
+    requests [lo, hi) (every tensor's leading dim), or, for a single request, KV heads [lo, hi) with A
+    replicated (SURVEY 8(e)).  The views are contiguous, so they can be handed to the C ABI as they are;
+    on a real N-GPU run each rank allocates exactly these shapes itself.  Returns a LayerState."""
+    import dataclasses as dc
+
+    from .state import LayerState
+    S = state.shape
+    r0, r1 = p.requests
+    h0, h1 = p.kv_heads
+    if p.mode == "kv_head" and S.batch != 1:
+        raise ValueError("KV-head shards are views of a single-request state")
+    lens = S.ctx_lens[r0:r1] if S.ctx_lens is not None else None
+    shape = dc.replace(S, batch=r1 - r0, n_kv_heads=h1 - h0, n_q_heads=(h1 - h0) * (S.n_q_heads // S.n_kv_heads),
+                       ctx_lens=lens)
+    req = lambda t: None if t is None else t[r0:r1]
+    head = lambda t: None if t is None else t[r0:r1, h0:h1]
+    t = dict(A=req(state.A), B=head(state.B), landmarks=head(state.landmarks), outlier_ids=head(state.outlier_ids),
+             K_out=head(state.K_out), V_out=head(state.V_out), K_win=head(state.K_win), V_win=head(state.V_win),
+             V_host=head(state.V_host), A_gen=req(state.A_gen), vc_values=head(state.vc_values),
+             vc_dir=head(state.vc_dir), vc_stats=head(state.vc_stats))
+    for k, v in t.items():
+        if v is not None and not v.is_contiguous():
+            raise ValueError(f"shard view of {k} is not contiguous")
+    return LayerState.from_tensors(shape, state.A.device, **t)

@@ -106,6 +106,22 @@ class LayerState:
             self.vc_dir = torch.zeros(b, hk, S.n_c, dtype=torch.int64, device=device)
             self.vc_stats = torch.zeros(b, hk, 4, dtype=torch.int64, device=device)
 
+    @classmethod
+    def from_tensors(cls, shape: Shape, device, **tensors) -> "LayerState":
+        """A LayerState over caller-provided tensors (e.g. shard views, shard.shard_state); no allocation
+        except the ragged-length arrays."""
+        self = cls.__new__(cls)
+        self.shape = shape
+        bd.ensure_init(device)
+        self.lens_host = self.lens_dev = None
+        if shape.ctx_lens is not None:
+            self.lens_host = torch.tensor(shape.ctx_lens, dtype=torch.int32)
+            self.lens_dev = self.lens_host.to(device)
+        for k in ("A", "B", "landmarks", "outlier_ids", "K_out", "V_out", "K_win", "V_win", "V_host", "A_gen",
+                  "vc_values", "vc_dir", "vc_stats"):
+            setattr(self, k, tensors.get(k))
+        return self
+
     def layer(self) -> bd.SkvLayer:
         return bd.layer_struct(self.A, self.B, self.landmarks, self.outlier_ids, self.K_out, self.V_out,
                                self.K_win, self.V_win, self.V_host, self.vc_values, self.vc_dir, self.vc_stats,

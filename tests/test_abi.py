@@ -189,32 +189,29 @@ def test_shape_window_capacity_for_ragged_and_multi_query():
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_score_plan_every_config(lib, name):
     """The tcgen05 scorer has a launch plan for every BASELINE config on a 148-SM B200, within its static
-    limits (<= 256 tiles and <= 4 KV heads per CTA, <= 64 partial slots per KV head)."""
+    limits (<= 64 tiles of 128 landmarks and <= 4 KV heads per CTA's contiguous tile range)."""
     shp = Shape.from_config(synth.CONFIGS[name])
     grid, tpc, heads, cph = bd.shadowkv_score_plan(shp.dims(), 148)
     tph = -(-shp.n_c // 128)
-    assert 1 <= grid <= 2 * 148 and tpc <= 256 and heads <= 4 and 2 * cph <= 64
+    assert 1 <= grid and tpc <= 64 and heads <= 4
     assert grid * tpc >= shp.batch * shp.n_kv_heads * tph          # every tile is covered
 
 
-@pytest.mark.parametrize("ctx", [1 << 21, 1 << 22, 7 << 20])
+@pytest.mark.parametrize("ctx", [1 << 21, 1 << 22, (1 << 24) - 65536 - 8])
 def test_score_plan_long_single_request(lib, ctx):
-    """one request of 2M / 4M / 7M tokens (8 KV heads) used to overflow the scorer's
-    64-tile outlier bitmap once the partial-slot limit lowered the grid; the plan re-checks both limits."""
+    """one request of 2M / 4M tokens (8 KV heads) used to overflow the scorer's 64-tile outlier
+    bitmap once a partial-slot limit lowered the grid.  The softmax partials are now per tile (no slot
+    limit), so the grid only grows: the tile bound holds at any length the ABI accepts."""
     d = _dims(ctx_len=ctx, budget=ctx // 512, n_outlier=48, window_cap=64)
     grid, tpc, heads, cph = bd.shadowkv_score_plan(d, 148)
-    assert tpc <= 256 and heads <= 4 and 2 * cph <= 64
+    assert tpc <= 64 and heads <= 4
     assert grid * tpc >= 8 * -(-((ctx - 16) // 8) // 128)
 
 
-def test_score_plan_rejects_what_no_grid_fits(lib):
-    """Beyond the kernel's limits the plan (and decode_step) says SKV_EUNSUPPORTED instead of
-    launching a kernel that would overrun its shared-memory bitmap."""
-    d = _dims(ctx_len=(1 << 24) - 65536 - 8, budget=1024, n_outlier=48, window_cap=64)
-    assert lib.shadowkv_score_plan(ctypes.byref(d), 148, (ctypes.c_int32 * 4)()) == bd.SKV_EUNSUPPORTED
-    assert "tiles" in lib.shadowkv_last_error().decode()
+def test_score_plan_argument_errors(lib):
     ok = _dims()
     assert lib.shadowkv_score_plan(ctypes.byref(ok), 0, (ctypes.c_int32 * 4)()) == bd.SKV_EINVAL
+    assert lib.shadowkv_score_plan(ctypes.byref(_dims(budget=0)), 148, (ctypes.c_int32 * 4)()) == bd.SKV_EINVAL
 
 
 def test_decode_needs_init_before_any_cuda(lib):

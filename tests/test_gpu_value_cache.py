@@ -13,7 +13,7 @@ import torch
 
 import synth
 from oracle import shadowkv_oracle as O
-from tests.parity import Problem
+from tests.parity import Problem, check_decode
 
 pytestmark = pytest.mark.gpu
 
