@@ -21,11 +21,14 @@
 // Kernels after the first are launched with programmatic dependent launch (PDL).
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "append.cuh"
 #include "kernels.h"
 #include "topk.cuh"
+#include "umma.cuh"
 
 namespace skv {
 
@@ -543,26 +546,30 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
 // =============================================================================================
 // a4 + a5 + a6: fused rebuild + host gather + attention over one unit of <= 64 tokens
 // =============================================================================================
-struct AttnSmem {      // byte offsets into dynamic smem
-  int v, a, bmat, q, p, tok, bytes;
+struct AttnSmem {      // byte offsets from the 1024-aligned base of dynamic smem
+  int a, bmat, v, q, pp, p, tok, bytes;
 };
-constexpr int kKStride = kHeadDim + 4;            // fp32 key tile row stride (floats; +4 against bank conflicts)
-constexpr int kBStride = kHeadDim + 8;            // B_h row stride in smem (bf16; 272 B rows: the 8 rows an
-                                                  // ldmatrix.trans phase reads fall in distinct banks)
+// A tile: the unit's 64 gathered factor rows A[t][0:r] as UMMA K-major SWIZZLE_128B atoms (TMA boxes of
+// 8 rows x 64 columns, 1 KB each; K block kb at a + kb * 8 KB, chunk c at + c * 1 KB).  The M = 128
+// MMA also reads rows 64..127 (TMEM lanes 64..127, never used): the 8 KB after the last K block must be
+// addressable smem (B_h follows).  Outlier / window units reuse the region for their exact K tile.
+// B_h: [r][128] MN-major SWIZZLE_128B, two TMA boxes of r rows x 64 columns (LBO = r * 128 B apart).
 __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
   AttnSmem s;
+  const int nkb = (r + 63) / 64;
   int off = 0;
-  s.v = off; off += kUnitTok * kHeadDim * 2;                                 // V tile bf16
-  s.a = off; { int ab = kUnitTok * r * 2; off += ab > kUnitTok * kHeadDim * 2 ? ab : kUnitTok * kHeadDim * 2; }  // A rows | K tile
-  s.bmat = off;                                                             // B_h; [a, bmat end) also holds
-  { const int bb = r * kBStride * 2, tile = kUnitTok * kKStride * 4 - (off - s.a);   // the fp32 rebuilt tile
-    off += bb > tile ? bb : tile; }
+  s.a = off; off += nkb * 8192 > kUnitTok * kHeadDim * 2 ? nkb * 8192 : kUnitTok * kHeadDim * 2;
+  s.bmat = off; off += 2 * r * 128;
+  if (off < nkb * 8192 + 8192) off = nkb * 8192 + 8192;
+  s.v = off; off += kUnitTok * kHeadDim * 2;                                // V tile bf16
   s.q = off; off += G * kHeadDim * 4;                                       // q fp32
+  s.pp = off; off += 2 * G * kUnitTok * 4;                                  // logit halves (two column sets)
   s.p = off; off += G * kUnitTok * 4;                                       // logits / probs
   s.tok = off; off += kUnitTok * 4;
-  s.bytes = off;
+  s.bytes = off + 1024;                                                     // + base alignment slack
   return s;
 }
+constexpr uint32_t kIdescRebuild = umma_idesc_bf16(128, 128, false, true);   // A K-major, B_h MN-major
 
 // a6 combine: out_hq = sum_s w_s o_s with w_s = exp(m_s - M) / sum_s' l_s' exp(m_s' - M) over the
 // per-unit partials (m_s, l_s, o_s) of one q head (split-KV log-sum-exp merge, fixed order).  A grid
@@ -642,67 +649,80 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
   }
 }
 
-// K~[64][128] = A_rows[64][r] . B_h[r][128]  (Alg 2 "MatMul(Gather(A, I), B)") with warp MMAs;
-// all 8 warps; result fp32 in Kt[64][kKStride], which aliases A_rows / B_h (synchronised here)
-__device__ __forceinline__ void rebuild_tile_mma(const uint16_t* As, const uint16_t* Bs, int r, float* Kt) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = (warp & 3) * 16, n0 = (warp >> 2) * 64;
-  float c[8][4];
+// RoPE (R15) of one token row held as two 32-column blocks x0 = cols [c0, c0+32), x1 = cols [c1, c1+32)
+// of the rebuilt key.  The column sets are chosen so that every rotation pair lies in one thread:
+// halves layout with rot = 128 (Llama): set s holds cols [32s, 32s+32) and their partners +64;
+// rot <= 64 (halves, rot/2 in {8, 16, 32}) or interleaved: set s holds [64s, 64s+64).
+__device__ __forceinline__ void rope_row(float* x0, float* x1, int c0, int c1, int t, const Rope& R) {
+  if (R.interleaved) {
 #pragma unroll
-  for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.f;
-  const uint32_t a_base = smem_u32(As + (m0 + (lane & 15)) * r + (lane >> 4) * 8);
-  const uint32_t b_base = smem_u32(Bs + (lane & 15) * kBStride + n0 + (lane >> 4) * 8);
-  for (int k0 = 0; k0 < r; k0 += 16) {
-    uint32_t a[4];
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]) : "r"(a_base + k0 * 2));
+    for (int blk = 0; blk < 2; ++blk) {
+      float* x = blk ? x1 : x0;
+      const int cb = blk ? c1 : c0;
 #pragma unroll
-    for (int nt = 0; nt < 8; nt += 2) {
-      uint32_t b[4];
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
-                   : "r"(b_base + (k0 * kBStride + nt * 8) * 2));
+      for (int e = 0; e < 32; e += 2) {
+        if (cb + e < R.rot) {
+          float sn, cs;
+          rope_sincos(t, __ldg(R.inv_freq + ((cb + e) >> 1)), &sn, &cs);
+          const float a = x[e], b = x[e + 1];
+          x[e] = a * cs - b * sn;
+          x[e + 1] = b * cs + a * sn;
+        }
+      }
+    }
+    return;
+  }
+  const int half = R.rot >> 1;
+  auto rot2 = [&](float& a, float& b, int i) {
+    float sn, cs;
+    rope_sincos(t, __ldg(R.inv_freq + i), &sn, &cs);
+    const float x = a, y = b;
+    a = x * cs - y * sn;
+    b = y * cs + x * sn;
+  };
+  if (half == 64) {                                     // pairs (c0 + e, c0 + 64 + e) = (x0[e], x1[e])
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2)
-        asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
-                     "{%8, %9}, {%0, %1, %2, %3};"
-                     : "+f"(c[nt + h2][0]), "+f"(c[nt + h2][1]), "+f"(c[nt + h2][2]), "+f"(c[nt + h2][3])
-                     : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[2 * h2]), "r"(b[2 * h2 + 1]));
+    for (int e = 0; e < 32; ++e) rot2(x0[e], x1[e], c0 + e);
+  } else if (c0 == 0) {                                 // set 0 holds every rotary dim (rot <= 64)
+    if (half == 32) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) rot2(x0[e], x1[e], e);
+    } else if (half == 16) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) rot2(x0[e], x0[e + 16], e);
+    } else if (half == 8) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rot2(x0[e], x0[e + 8], e);
     }
   }
-  __syncthreads();                                       // every warp has read A rows and B_h
-  const int g = lane >> 2, cq = (lane & 3) * 2;
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    const int col = n0 + t * 8 + cq;
-    *reinterpret_cast<float2*>(Kt + (m0 + g) * kKStride + col) = make_float2(c[t][0], c[t][1]);
-    *reinterpret_cast<float2*>(Kt + (m0 + g + 8) * kKStride + col) = make_float2(c[t][2], c[t][3]);
-  }
-  __syncthreads();
 }
 
 template <int G>
 __global__ void __launch_bounds__(256, 2)
-k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t* __restrict__ sel,
-              int* __restrict__ flags, int step,
+k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmG, Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q,
+              int32_t* __restrict__ sel, int* __restrict__ flags, int step,
               float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
               int n_gen_u, int n_split, float scale, uint16_t* __restrict__ dbg, int early_next) {
   TRACE_INIT;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
   const AttnSmem lay = attn_smem_layout(D.r, G);
   uint16_t* Vs = reinterpret_cast<uint16_t*>(smem + lay.v);
-  uint16_t* As = reinterpret_cast<uint16_t*>(smem + lay.a);     // A rows [64][r]  or K tile [64][128]
-  uint16_t* Bs = reinterpret_cast<uint16_t*>(smem + lay.bmat);  // [r][128]
-  float* qs = reinterpret_cast<float*>(smem + lay.q);           // [G][128]
-  float* P = reinterpret_cast<float*>(smem + lay.p);            // [G][64]
+  uint8_t* As = smem + lay.a;                                  // A tile (SW128) or exact K tile [64][128]
+  uint8_t* Bs = smem + lay.bmat;                               // B_h (MN-major SW128)
+  float* qs = reinterpret_cast<float*>(smem + lay.q);          // [G][128]
+  float* Pp = reinterpret_cast<float*>(smem + lay.pp);         // [2][G][64]
+  float* P = reinterpret_cast<float*>(smem + lay.p);           // [G][64]
   int* tok = reinterpret_cast<int*>(smem + lay.tok);
-  __shared__ __align__(8) uint64_t barAB, barV;
+  __shared__ __align__(8) uint64_t barAB, barV, barMMA;
+  __shared__ uint32_t tmem_base;
   __shared__ float2 ml[G];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane & 15;
-  const int d = tid & 127, hh = tid >> 7;                      // PV / merge ownership: dim, head parity
   const int BH = D.b * D.hk;
   const int stp0 = cur_step(D, step);
   const int T_out = D.o * kChunk;
+  const int nkb = (D.r + 63) >> 6;
   int T_win;                                           // this request's window incl. the s_q new tokens
   // unit kinds: 0 selected chunks, 1 outliers, 2 window (plain: context tail + generated; low-rank: tail
   // only), 3 generated tokens rebuilt from their low-rank rows (NEXT-4)
@@ -731,44 +751,51 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
   }
   int32_t* slots = sel + (size_t)bh * D.k;                     // k_select's unordered selection (id + 1)
   const int nch = kind == 0 ? min(8, D.k - ui * 8) : 0;        // chunks of a selected-chunk unit (>= 1)
+  const bool rebuild = kind == 0 || kind == 3;
   trace(2, 0);
   if (tid == 0) {   // selected-chunk units: one arrival per chunk-issuing thread
-    mbar_init(&barAB, kind == 0 ? nch : 1); mbar_init(&barV, kind == 0 ? nch : 1); fence_mbar_init();
-    if (kind == 0 || kind == 3)                           // B_h's bytes, before any arrival can complete the phase
+    mbar_init(&barAB, kind == 0 ? nch : 1); mbar_init(&barV, kind == 0 ? nch : 1); mbar_init(&barMMA, 1);
+    fence_mbar_init();
+    if (rebuild)                                          // B_h's bytes, before any arrival can complete the phase
       asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;"
-                   :: "r"(smem_u32(&barAB)), "r"((uint32_t)(D.r * kHeadDim * 2)) : "memory");
+                   :: "r"(smem_u32(&barAB)), "r"((uint32_t)(2 * D.r * 128)) : "memory");
   }
+  if (rebuild && warp == 0) tmem_alloc<128>(&tmem_base);      // K~ accumulator: 128 lanes x 128 fp32 columns
   // q is a call input: stage it before waiting on the producer kernels
   for (int i = tid; i < G * kHeadDim; i += 256)
     qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
   int ntok;
   int vc_id = -1;                              // value cache: this thread's chunk and the call's generation
   unsigned long long vc_gen = 0;
-  const int tx = tid & 15, ty = tid >> 4;      // key-tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
+  const int tx = tid & 15, ty = tid >> 4;      // exact-key tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
   float acc[4][8];
-  if (kind == 0 || kind == 3) {
-    const size_t bbytes = (size_t)D.r * kHeadDim * 2;
-    // B_h does not depend on the selection: fetched before the PDL wait, one bulk copy per 256 B row into the
-    // padded layout, issued by warps 1..7 so that the chunk threads of warp 0 never queue behind them (the
-    // byte count was posted at barrier init, before any arrival)
-    (void)bbytes;
-    if (warp >= 1)
-      for (int i = tid - 32; i < D.r; i += 256 - 32)
-        bulk_g2s(Bs + i * kBStride, Ly.B + ((size_t)bh * D.r + i) * kHeadDim, kHeadDim * 2, &barAB);
+  if (rebuild) {
+    // B_h does not depend on the selection: two TMA boxes (64 columns x r rows) issued at once by a thread
+    // of warp 1, so the chunk threads of warp 0 never queue behind them
+    if (tid == 32) {
+      prefetch_tensormap(&tmB);
+      tma_load_2d(Bs, &tmB, 0, bh * D.r, &barAB);
+      tma_load_2d(Bs + D.r * 128, &tmB, 64, bh * D.r, &barAB);
+    }
     if (kind == 3) {  // generated tokens g0 .. g0+ntok-1: low-rank rows + values, positions s_b + g (R16)
       const int g0 = ui * kUnitTok, nt = min(kUnitTok, n_gen - g0);
       cta_wait_flag(&flags[(size_t)bh * 4]);                    // (score's a7 projection is visible)
       if (tid == 0) {
-        mbar_expect_tx(&barAB, nt * D.r * 2);
-        bulk_g2s(As, D.lr_A + ((size_t)b * D.wcap + g0) * D.r, nt * D.r * 2, &barAB);
+        const int nblk = (nt + 7) >> 3;
+        mbar_expect_tx(&barAB, nblk * nkb * 1024);
+        for (int blk = 0; blk < nblk; ++blk)
+          for (int kb = 0; kb < nkb; ++kb)
+            tma_load_2d(As + kb * 8192 + blk * 1024, &tmG, kb * 64, b * D.wcap + g0 + blk * 8, &barAB);
         mbar_expect_tx(&barV, nt * kHeadDim * 2);
         bulk_g2s(Vs, Ly.V_win + ((size_t)bh * D.wcap + req_weff(D, b) + g0) * kHeadDim, nt * kHeadDim * 2, &barV);
       }
       if (tid < kUnitTok) tok[tid] = tid < nt ? req_s(D, b) + g0 + tid : 0;
     }
-    // thread c < nch waits for its slot, then issues its chunk's two copies at once: the value fetch
-    // of each chunk starts the moment k_select publishes it
+    // thread c < nch waits for its slot, then issues its chunk's copies at once: the value fetch of each
+    // chunk starts the moment k_select publishes it
     if (kind == 0 && tid < nch) {                        // (generated units set their positions above)
       const int* sp = slots + ui * 8 + tid;
       int v;
@@ -777,10 +804,10 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       vc_id = id;
 #pragma unroll
       for (int e = 0; e < kChunk; ++e) tok[tid * kChunk + e] = id * kChunk + e;
-      const uint32_t rb = kChunk * D.r * 2;
-      // a4 operands (HBM): 8 contiguous factor rows (2.5 KB at r = 160)
-      mbar_expect_tx(&barAB, rb);
-      bulk_g2s(As + tid * kChunk * D.r, Ly.A + ((size_t)b * D.s + (size_t)id * kChunk) * D.r, rb, &barAB);
+      // a4 operands (HBM): the chunk's 8 factor rows A[t][0:r] as nkb SWIZZLE_128B boxes (TMA tensor copies)
+      mbar_expect_tx(&barAB, nkb * 1024);
+      for (int kb = 0; kb < nkb; ++kb)
+        tma_load_2d(As + kb * 8192 + tid * 1024, &tmA, kb * 64, b * D.s + id * kChunk, &barAB);
       // a5: the value chunk straight from pinned host memory over PCIe (zero-copy bulk copy) -- or,
       // with the value cache, from HBM when the chunk was selected in the previous step ("index
       // scan to detect the missed chunks": one directory probe per selected chunk, R26)
@@ -804,59 +831,40 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     ntok = kind == 0 ? nch * kChunk : min(kUnitTok, n_gen - ui * kUnitTok);
     if (early_next) pdl_trigger();                       // next layer's score may become resident
     trace(2, 2);
-    __syncthreads();
     if (D.serial) mbar_wait(&barV, 0);                   // SKV_SERIALIZE: values first, then the rebuild
-    mbar_wait(&barAB, 0);
-    trace(2, 3);
-    // ---- K~ = A_rows . B_h on the tensor cores (bf16 x bf16 -> fp32, mma.sync m16n8k16): a 64 x 128 x r
-    //      GEMM per unit, warp w owns rows 16 (w % 4).., columns 64 (w / 4)..; the fp32 tile goes through
-    //      smem (over the consumed A rows / B_h) into the per-thread layout of the RoPE / logits code
-    {
-      float* Kt = reinterpret_cast<float*>(As);
-      rebuild_tile_mma(As, Bs, D.r, Kt);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4* src = reinterpret_cast<const float4*>(Kt + (ty + 16 * i) * kKStride + tx * 8);
-        const float4 v0 = src[0], v1 = src[1];
-        acc[i][0] = v0.x; acc[i][1] = v0.y; acc[i][2] = v0.z; acc[i][3] = v0.w;
-        acc[i][4] = v1.x; acc[i][5] = v1.y; acc[i][6] = v1.z; acc[i][7] = v1.w;
-      }
+    // ---- K~ = A_rows . B_h on the 5th-generation tensor cores (Alg 2 "MatMul(Gather(A, I), B)"):
+    //      one thread issues r/16 tcgen05.mma (M = 128 rows of which 64 are the unit's tokens, N = 128, K = 16
+    //      each) into an fp32 TMEM accumulator; completion is committed to barMMA
+    const uint32_t tmem = tmem_base;
+    if (tid == 0) {
+      mbar_wait(&barAB, 0);
+      tc_fence_after();
+      trace(2, 3);
+      const uint32_t a0 = smem_u32(As), b0 = smem_u32(Bs), lbo = (uint32_t)D.r * 128u;
+      for (int ks = 0; ks < (D.r >> 4); ++ks)
+        umma_f16(tmem, umma_desc_sw128(a0 + (ks >> 2) * 8192 + (ks & 3) * 32), umma_desc_sw128_mn(b0 + ks * 2048, lbo),
+                 kIdescRebuild, ks > 0);
+      umma_commit(&barMMA);
     }
-    // ---- RoPE at the tokens' absolute positions (R15), in registers
-    const int halfrot = R.rot >> 1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int t = tok[ty + 16 * i];
-      if (R.interleaved) {
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const int d0 = tx * 8 + e;
-          if (d0 < R.rot) {
-            float sn, cs;
-            rope_sincos(t, R.inv_freq[d0 >> 1], &sn, &cs);
-            const float x0 = acc[i][e], x1 = acc[i][e + 1];
-            acc[i][e] = x0 * cs - x1 * sn;
-            acc[i][e + 1] = x1 * cs + x0 * sn;
-          }
-        }
-      } else {
-        const int sh = halfrot >> 3;                       // partner lane offset (halfrot % 8 == 0)
-        const bool lowh = tx * 8 < halfrot, inrot = tx * 8 < R.rot;
-        const int src = (lane & 16) | (lowh ? tx + sh : tx - sh) & 15;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float pv = __shfl_sync(0xffffffffu, acc[i][e], inrot ? src : lane);
-          if (inrot) {
-            const int pi = (lowh ? tx * 8 : tx * 8 - halfrot) + e;
-            float sn, cs;
-            rope_sincos(t, R.inv_freq[pi], &sn, &cs);
-            acc[i][e] = lowh ? acc[i][e] * cs - pv * sn : acc[i][e] * cs + pv * sn;
-          }
-        }
-      }
+    __syncwarp();
+    // ---- epilogue: warps 0, 1, 4, 5 read TMEM lanes 0..63 (one token row per thread, lane quadrant =
+    //      warp % 4); the two warps of a row split its 128 columns into RoPE-closed sets (rope_row)
+    float x0[32], x1[32];
+    const int erow = 32 * (warp & 1) + lane, eset = warp >> 2;
+    const bool hl = !R.interleaved && R.rot > 64;
+    const int c0 = hl ? 32 * eset : 64 * eset, c1 = hl ? 64 + 32 * eset : 64 * eset + 32;
+    const bool epi = (warp & 2) == 0;
+    if (epi) {
+      mbar_wait(&barMMA, 0);
+      tc_fence_after();
+      const uint32_t tr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+      tmem_ld32(tr + c0, x0);
+      tmem_ld32(tr + c1, x1);
+      rope_row(x0, x1, c0, c1, tok[erow], R);          // RoPE at the token's absolute position (R15, R16)
     }
     if (dbg && kind == 0) {   // a4 parity hook: bf16 of the fp32 keys at the chunk's rank in the ascending selection
-      __syncthreads();                                   // A rows consumed: reuse their smem for the ids
+      mbar_wait(&barMMA, 0);                             // the MMA has consumed the A tile: reuse it for the ids
+      __syncthreads();
       int* ids = reinterpret_cast<int*>(As);
       for (int i = tid; i < D.k; i += 256) {
         int v;
@@ -864,24 +872,51 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
         ids[i] = v - 1;
       }
       __syncthreads();
+      if (epi && erow < ntok) {
+        const int cid = tok[erow] >> 3;
+        int pos = 0;
+        for (int c = 0; c < D.k; ++c) pos += ids[c] < cid;
+        uint16_t* drow = dbg + (((size_t)bh * D.k + pos) * kChunk + (erow & 7)) * kHeadDim;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = ty + 16 * i;
-        if (row < ntok) {
-          const int cid = tok[row] >> 3;
-          int pos = 0;
-          for (int c = 0; c < D.k; ++c) pos += ids[c] < cid;
-          uint4 kb = make_uint4(pack_bf2(acc[i][0], acc[i][1]), pack_bf2(acc[i][2], acc[i][3]),
-                                pack_bf2(acc[i][4], acc[i][5]), pack_bf2(acc[i][6], acc[i][7]));
-          *reinterpret_cast<uint4*>(dbg + (((size_t)bh * D.k + pos) * kChunk + (row & 7)) * kHeadDim + tx * 8) = kb;
+        for (int e = 0; e < 32; e += 8) {
+          *reinterpret_cast<uint4*>(drow + c0 + e) = make_uint4(pack_bf2(x0[e], x0[e + 1]), pack_bf2(x0[e + 2], x0[e + 3]),
+                                                                pack_bf2(x0[e + 4], x0[e + 5]), pack_bf2(x0[e + 6], x0[e + 7]));
+          *reinterpret_cast<uint4*>(drow + c1 + e) = make_uint4(pack_bf2(x1[e], x1[e + 1]), pack_bf2(x1[e + 2], x1[e + 3]),
+                                                                pack_bf2(x1[e + 4], x1[e + 5]), pack_bf2(x1[e + 6], x1[e + 7]));
         }
       }
+    }
+    // ---- logits q . k~ (fp32 keys), half a row per thread, combined below in a fixed order
+    if (epi) {
+#pragma unroll 4
+      for (int hq = 0; hq < G; ++hq) {
+        const float* qh = qs + hq * kHeadDim;
+        float a = 0.f, bsum = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 qa = *reinterpret_cast<const float4*>(qh + c0 + e);
+          const float4 qb = *reinterpret_cast<const float4*>(qh + c1 + e);
+          a = fmaf(x0[e], qa.x, a); a = fmaf(x0[e + 1], qa.y, a); a = fmaf(x0[e + 2], qa.z, a); a = fmaf(x0[e + 3], qa.w, a);
+          bsum = fmaf(x1[e], qb.x, bsum); bsum = fmaf(x1[e + 1], qb.y, bsum);
+          bsum = fmaf(x1[e + 2], qb.z, bsum); bsum = fmaf(x1[e + 3], qb.w, bsum);
+        }
+        Pp[(eset * G + hq) * kUnitTok + erow] = a + bsum;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < G * kUnitTok; idx += 256) {
+      const int hq = idx / kUnitTok, row = idx - hq * kUnitTok;
+      // generated low-rank unit: token g = ui*64 + row is seen by query row hq (token i = hq % s_q) iff
+      // g <= step + i (causal, R28)
+      const bool vis = row < ntok && (kind == 0 || ui * kUnitTok + row < stp0 + 1 + hq % D.sq);
+      P[idx] = vis ? (Pp[hq * kUnitTok + row] + Pp[(G + hq) * kUnitTok + row]) * scale : -INFINITY;
     }
   } else {
     // ---- outlier or window (R8, R18) unit: exact keys and values from HBM
     if (early_next) pdl_trigger();
     cta_wait_flag(&flags[(size_t)bh * 4]);              // (score's window append is visible)
     const uint16_t *Ksrc, *Vsrc;
+    uint16_t* Ks = reinterpret_cast<uint16_t*>(As);
     if (kind == 1) {
       ntok = min(kUnitTok, T_out - ui * kUnitTok);
       Ksrc = Ly.K_out + ((size_t)bh * T_out + ui * kUnitTok) * kHeadDim;
@@ -901,7 +936,7 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     }
     if (tid == 0) {
       mbar_expect_tx(&barAB, ntok * kHeadDim * 2);
-      bulk_g2s(As, Ksrc, ntok * kHeadDim * 2, &barAB);
+      bulk_g2s(Ks, Ksrc, ntok * kHeadDim * 2, &barAB);
       mbar_expect_tx(&barV, ntok * kHeadDim * 2);
       bulk_g2s(Vs, Vsrc, ntok * kHeadDim * 2, &barV);
     }
@@ -909,15 +944,13 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int row = ty + 16 * i;
-      if (row < ntok) unpack8(*reinterpret_cast<const uint4*>(As + row * kHeadDim + tx * 8), acc[i]);
+      if (row < ntok) unpack8(*reinterpret_cast<const uint4*>(Ks + row * kHeadDim + tx * 8), acc[i]);
       else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
       }
     }
-  }
-  // ---- logits q . k for G heads: 4 tokens x (<= 4 heads) per lane per pass, reduced over 16 lanes
-  {
+    // ---- logits q . k for G heads: 4 tokens x (<= 4 heads) per lane per pass, reduced over 16 lanes
     constexpr int HC = G < 4 ? G : 4;
 #pragma unroll
     for (int h0 = 0; h0 < G; h0 += HC) {
@@ -941,9 +974,8 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
       if (sub < 4 * HC) {
         const int i = sub / HC, hq = h0 + sub % HC, row = ty + 16 * i;
         // window unit: query row hq (token i = hq % s_q) sees new tokens 0..i only (causal, R28)
-        // (generated low-rank unit: token g = ui*64 + row likewise sees g <= step + i)
-        const bool vis = row < ntok && (kind == 0 || kind == 1 || (kind == 2 && lowrank) ||
-                                        ui * kUnitTok + row < (kind == 2 ? T_win - D.sq : stp0) + 1 + hq % D.sq);
+        const bool vis = row < ntok && (kind == 1 || (kind == 2 && lowrank) ||
+                                        ui * kUnitTok + row < T_win - D.sq + 1 + hq % D.sq);
         P[hq * kUnitTok + row] = vis ? pv[0] * scale : -INFINITY;
       }
     }
@@ -995,6 +1027,11 @@ k_sparse_attn(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q, int32_t*
     }
   }
   if (vc_id >= 0 && Ly.vc_dir) bulk_wait_read();         // the cache write-back has read its smem
+  if (rebuild) {                                         // every TMEM read finished (tcgen05.ld waited)
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem_base);
+  }
   trace(2, 8);
 }
 
@@ -1110,6 +1147,20 @@ cudaError_t init_decode_attrs() {
   return cudaSuccess;
 }
 
+// 2D bf16 tensor map [outer][inner] (row pitch inner * 2 bytes), box {box_inner, box_outer}, SWIZZLE_128B
+static bool encode_bf16_2d(const DevCtx& ctx, CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                           uint32_t box_inner, uint32_t box_outer) {
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {inner, outer};
+  const cuuint64_t gstride[1] = {inner * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int G>
 static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                                    const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
@@ -1170,8 +1221,15 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   // tuning hook: SKV_SPARSE_TRIGGER=0 keeps the implicit trigger at CTA exit (the next layer's score
   // grid then launches only when this grid drains)
   const int early_next = tuning().early_next;
+  // TMA tensor maps of the rebuild's operands: A [b*s][r] and A_gen [b*wcap][r] in 8-row x 64-column
+  // SWIZZLE_128B boxes (one chunk's K block), B [b*h_kv*r][128] in r-row x 64-column boxes (MN-major)
+  CUtensorMap tmA, tmB, tmG;
+  if (!encode_bf16_2d(ctx, &tmA, Ly.A, D.r, (uint64_t)D.b * D.s, 64, 8) ||
+      !encode_bf16_2d(ctx, &tmB, Ly.B, kHeadDim, (uint64_t)D.b * D.hk * D.r, 64, D.r) ||
+      !encode_bf16_2d(ctx, &tmG, D.lr_A ? D.lr_A : Ly.A, D.r, D.lr_A ? (uint64_t)D.b * D.wcap : (uint64_t)D.b * D.s, 64, 8))
+    return cudaErrorInvalidValue;
   nvtxRangePushA("skv::sparse_attn");
-  e = launch_pdl(!D.serial, k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, D, R, Ly, q,
+  e = launch_pdl(!D.serial, k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, tmA, tmB, tmG, D, R, Ly, q,
                       ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
                       n_sel_u, n_out_u, n_win_u, n_gen_u, n_split, scale, dbg_keys, early_next);
   nvtxRangePop();

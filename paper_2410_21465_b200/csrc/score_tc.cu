@@ -21,6 +21,7 @@
 #include "append.cuh"
 #include "common.cuh"
 #include "kernels.h"
+#include "umma.cuh"
 
 namespace skv {
 
@@ -34,60 +35,15 @@ constexpr int kTcThreads = 352;         // 2 x 4 epilogue warps, 1 TMA producer,
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
 
-// Landmarks are streamed once per decode step and never re-read within it: load them with an L2
+// Landmarks are streamed once per decode step and never re-read within it: they are loaded with an L2
 // evict-first policy so that they do not push the freshly written logits (re-read by k_select) and
 // the small per-step state out of L2 (c3/c5 stream 0.2-2 GB of landmarks per layer through 126 MB).
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t p; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p;
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                            uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;"
-      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
-// UMMA shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);          // start address      [0,14)
-  d |= (uint64_t)1u << 16;                          // LBO (unused for swizzled K-major) [16,30)
-  d |= (uint64_t)(1024u >> 4) << 32;                // SBO = 1024 B       [32,46)
-  d |= (uint64_t)1u << 46;                          // version = 1 (Blackwell) [46,48)
-  d |= (uint64_t)2u << 61;                          // layout = SWIZZLE_128B   [61,64)
-  return d;
-}
 
 // kind::f16 instruction descriptor: A,B bf16 K-major, D fp32, M = 128, N = 16.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdesc = umma_idesc_bf16(128, 16, false, false);
 
-__device__ __forceinline__ void umma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-      :: "r"(dtmem), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-               :: "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ bool in_sorted(const int32_t* ids, int o, int j) {
@@ -139,7 +95,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     for (int s = 0; s < kTcStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < kTcAcc; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
     fence_mbar_init();
-    asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    prefetch_tensormap(&tmap);
   }
   if (warp == 0 && ntile > 0) {                        // TMEM: 8 accumulator buffers x 16 fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" :: "r"(smem_u32(&tmem_base)));
@@ -231,7 +187,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         for (int k = 0; k < kHeadDim / 16; ++k) {
           const uint32_t koff = (k >> 2) * (kTileBytes / 2) + (k & 3) * 32;
           const uint32_t kboff = (k >> 2) * 2048 + (k & 3) * 32;
-          umma_f16(tmem + buf * 16, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + kboff), k > 0);
+          umma_f16(tmem + buf * 16, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + kboff), kIdesc, k > 0);
         }
         umma_commit(&empty[s]);          // smem stage may be refilled once these MMAs retire
         umma_commit(&acc_full[buf]);     // accumulator ready for the epilogue

@@ -62,7 +62,10 @@ def test_value_cache_parity_and_hits(name):
         gout, gsel, gkeys = P.gpu_decode(t, si)
         rout, rsel, _ = P.gpu_decode(t, si, st=ref)
         assert np.array_equal(gout, rout) and np.array_equal(gsel, rsel), f"cache changed the result at step {t}"
-        _, ost = P.check(ost, t, si, (gout, gsel, gkeys))
+        ost0 = ost
+        oout, osel, oz, okeys, ost = P.oracle_decode(ost, t, si)
+        check_decode(cfg, gout, gsel, gkeys, oout, osel, oz, okeys,
+                     rerun=lambda s_, ost0=ost0, t=t, si=si: P.oracle_decode(ost0, t, si, sel=s_))
         stats = P.st.cache_stats().numpy()
         assert (stats[..., 0] == t + 1).all()                      # one generation per decode step
         for bi in range(b):
