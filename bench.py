@@ -595,6 +595,13 @@ def run_ours(args, cfg):
         del inp
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
+    # Alg 1 minus the SVD (a0, untimed setup): one layer's shadowkv_build_cache, CUDA events, median of 5
+    bms = []
+    for _ in range(5):
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(); states[0].build(rope.struct, ws); b1.record(); b1.synchronize()
+        bms.append(b0.elapsed_time(b1))
+    build_ms = statistics.median(bms)
 
     # --- per-step inputs (fresh q every step and layer => fresh selections, alpha ~ 0) --------
     def step_inputs(i, device):
@@ -788,7 +795,8 @@ def run_ours(args, cfg):
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
             "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
-            "setup_s": setup_s}
+            "setup_s": setup_s,
+            "build_ms_per_layer": build_ms}
     # P:200-206 equivalent bandwidth of the uncached step (alpha = 0): dense KV bytes / layer time, and the
     # paper's model with this box's bandwidths
     S_, C_, K_, O_ = cfg.ctx_len, cfg.chunk, cfg.budget, cfg.n_outlier

@@ -98,8 +98,8 @@ typedef struct {
 
 typedef struct {
   int32_t rotary_dim;     /* even, 2 <= rotary_dim <= d; dims >= rotary_dim pass through (R15);
-                             halves layout additionally needs rotary_dim/2 % 8 == 0 (else
-                             SKV_EUNSUPPORTED)                                                  */
+                             halves layout additionally needs rotary_dim in {16, 32, 64, 128}
+                             (else SKV_EUNSUPPORTED)                                            */
   int32_t interleaved;    /* 0: halves layout (x_i, x_{i+rot/2}) [Llama]; 1: pairs (2i, 2i+1) [GLM] */
   const float *inv_freq;  /* device, rotary_dim/2 fp32; angle = fl32(fl32(t) * inv_freq[i])      */
 } skv_rope;

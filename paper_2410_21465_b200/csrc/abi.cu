@@ -118,8 +118,9 @@ skv_status check_rope(const skv_rope* r, int head_dim, skv::Rope* R) {
   if (r->rotary_dim < 2 || r->rotary_dim > head_dim || (r->rotary_dim & 1))
     return fail(SKV_EINVAL, "rotary_dim %d must be even and in [2, %d]", r->rotary_dim, head_dim);
   if (!r->inv_freq) return fail(SKV_EINVAL, "rope.inv_freq is NULL");
-  if (!r->interleaved && (r->rotary_dim / 2) % 8)
-    return fail(SKV_EUNSUPPORTED, "halves-layout rotary_dim %d: rotary_dim/2 must be a multiple of 8", r->rotary_dim);
+  if (!r->interleaved && r->rotary_dim != 16 && r->rotary_dim != 32 && r->rotary_dim != 64 && r->rotary_dim != 128)
+    return fail(SKV_EUNSUPPORTED, "halves-layout rotary_dim %d: must be 16, 32, 64 or 128 (rotation pairs of a key "
+                "row must fall in one thread's column set after the tcgen05 rebuild)", r->rotary_dim);
   *R = skv::Rope{r->inv_freq, r->rotary_dim, r->interleaved ? 1 : 0};
   return SKV_OK;
 }
@@ -293,7 +294,8 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
   if (K_rope && !aligned16(K_rope)) return fail(SKV_EINVAL, "K_rope is not 16-byte aligned");
-  if (!need_ctx()) return SKV_ESTATE;
+  const skv::DevCtx* ctx = need_ctx();
+  if (!ctx) return SKV_ESTATE;
   // V_host must be page-locked and device-mapped at the same address (UVA), P:136 V^CPU
   cudaPointerAttributes attr;
   cudaError_t e = cudaPointerGetAttributes(&attr, Ly.V_host);
@@ -309,7 +311,7 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
         (e = cudaMemsetAsync(Ly.vc_stats, 0, (size_t)D.b * D.hk * 4 * 8, s)) != cudaSuccess)
       return fail(SKV_ECUDA, "value-cache reset: %s", cudaGetErrorString(e));
   }
-  e = skv::launch_build(D, R, Ly, K_rope, ws, static_cast<cudaStream_t>(stream), &launches);
+  e = skv::launch_build(D, R, Ly, K_rope, ws, static_cast<cudaStream_t>(stream), &launches, *ctx);
   if (e != cudaSuccess) return fail(SKV_ECUDA, "build launch failed: %s", cudaGetErrorString(e));
   g_launches = launches;
   g_err.clear();

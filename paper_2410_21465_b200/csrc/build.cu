@@ -5,9 +5,14 @@
 //   k_build_select_outliers ArgTopK(-m, o) per (b, h): exact radix select, ties -> lower j (R12)
 //   k_build_outliers_window post-RoPE keys (bf16) + values (zero-copy from host) of the outlier
 //                           chunks and of the window tail (R8)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kernels.h"
 #include "keytile.cuh"
+#include "rope.cuh"
 #include "topk.cuh"
+#include "umma.cuh"
 
 namespace skv {
 
@@ -17,23 +22,109 @@ static __device__ __forceinline__ int* tile_tok_ptr(uint8_t* smem, int r) {
   return reinterpret_cast<int*>(smem + (ab > kt ? ab : kt));
 }
 
+// Key tile of the build on the 5th-generation tensor cores: K~[128 tokens][128] = A[t0.., :r] . B_h
+// (the keys the factors represent, Alg 1 / Alg 2 "MatMul(A, B)") with one tcgen05.mma
+// chain (M = 128 tokens, N = 128, K = r) into TMEM; RoPE in registers after tcgen05.ld (rope_row);
+// the fp32 post-RoPE keys go to smem [128][kKsStride] for the chunk statistics.
+// smem (1024-aligned): A tile [128 rows] K-major SWIZZLE_128B (TMA boxes of 128 rows x 64 columns, K
+// block kb at kb * 16 KB) | B_h MN-major SWIZZLE_128B (two boxes of r rows x 64 columns); the fp32 key
+// tile aliases both once the MMAs have completed.
+constexpr int kKsStride = kHeadDim + 4;               // floats: 528-byte rows, conflict-free 16 B stores
+__host__ __device__ constexpr size_t build_tc_smem_bytes(int r) {
+  const size_t ab = (size_t)((r + 63) / 64) * 16384 + (size_t)2 * r * 128;
+  const size_t ks = (size_t)kTileTok * kKsStride * 4;
+  return (ab > ks ? ab : ks) + kTileTok * sizeof(int) + 1024;
+}
+constexpr uint32_t kIdescBuild = umma_idesc_bf16(128, 128, false, true);
+
+__device__ __forceinline__ void build_key_tile_tc(const CUtensorMap* tmA, const CUtensorMap* tmB, int row0, int brow0,
+                                                  int r, const Rope& R, const int* tok, uint8_t* smem, float* Ks,
+                                                  uint64_t* bar_ab, uint64_t* bar_mma, uint32_t* tmem_slot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nkb = (r + 63) >> 6;
+  uint8_t* As = smem;
+  uint8_t* Bs = smem + nkb * 16384;
+  if (tid == 0) {
+    mbar_init(bar_ab, 1); mbar_init(bar_mma, 1); fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (tid == 0) {
+    mbar_expect_tx(bar_ab, nkb * 16384 + 2 * r * 128);
+    for (int kb = 0; kb < nkb; ++kb) tma_load_2d(As + kb * 16384, tmA, kb * 64, row0, bar_ab);
+    tma_load_2d(Bs, tmB, 0, brow0, bar_ab);
+    tma_load_2d(Bs + r * 128, tmB, 64, brow0, bar_ab);
+    mbar_wait(bar_ab, 0);
+    tc_fence_after();
+    const uint32_t a0 = smem_u32(As), b0 = smem_u32(Bs), lbo = (uint32_t)r * 128u;
+    for (int ks = 0; ks < (r >> 4); ++ks)
+      umma_f16(tmem, umma_desc_sw128(a0 + (ks >> 2) * 16384 + (ks & 3) * 32), umma_desc_sw128_mn(b0 + ks * 2048, lbo),
+               kIdescBuild, ks > 0);
+    umma_commit(bar_mma);
+  }
+  __syncwarp();
+  mbar_wait(bar_mma, 0);                                // (all threads: Ks below aliases the operands)
+  tc_fence_after();
+  const int row = 32 * (warp & 3) + lane, set = warp >> 2;
+  int c0, c1;
+  rope_col_sets(R, set, &c0, &c1);
+  float x0[32], x1[32];
+  const uint32_t tr = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+  tmem_ld32(tr + c0, x0);
+  tmem_ld32(tr + c1, x1);
+  rope_row(x0, x1, c0, c1, tok[row], R);
+  __syncthreads();                                      // every warp has read TMEM; operands are dead
+  float* kr = Ks + row * kKsStride;
+#pragma unroll
+  for (int e = 0; e < 32; e += 4) {
+    *reinterpret_cast<float4*>(kr + c0 + e) = make_float4(x0[e], x0[e + 1], x0[e + 2], x0[e + 3]);
+    *reinterpret_cast<float4*>(kr + c1 + e) = make_float4(x1[e], x1[e + 1], x1[e + 2], x1[e + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<128>(tmem);
+}
+
 __global__ void __launch_bounds__(kTileThreads)
-k_build_chunks(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ K_rope, float* __restrict__ mincos,
-               float* __restrict__ negm) {
-  extern __shared__ __align__(16) uint8_t smem[];
+k_build_chunks(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Dims D, Rope R,
+               Layer Ly, const uint16_t* __restrict__ K_rope, float* __restrict__ mincos, float* __restrict__ negm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
+  __shared__ __align__(8) uint64_t bar_ab, bar_mma;
+  __shared__ uint32_t tmem_slot;
   const int tile = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t bh = (size_t)b * D.hk + h;
   float* Ks = reinterpret_cast<float*>(smem);
-  int* tok = tile_tok_ptr(smem, D.r);
+  const size_t ab = (size_t)((D.r + 63) / 64) * 16384 + (size_t)2 * D.r * 128;
+  const size_t ksb = (size_t)kTileTok * kKsStride * 4;
+  int* tok = reinterpret_cast<int*>(smem + (ab > ksb ? ab : ksb));
   const int j0 = tile * 16;
   const int ncb = req_nc(D, b);                         // this request's grid (ragged batch)
   const int ntok = max(0, min(kTileTok, (ncb - j0) * kChunk));
   if (tid < kTileTok) tok[tid] = j0 * kChunk + tid;
-  __syncthreads();
-  produce_key_tile(Ly.A + (size_t)b * D.s * D.r, Ly.B + bh * D.r * kHeadDim,
-                   K_rope ? K_rope + bh * D.s * kHeadDim : nullptr, D.r, tok, ntok,
-                   RopeArgs{R.inv_freq, R.rot, R.interleaved}, smem, Ks);
+  if (K_rope) {                                         // given post-RoPE keys: widened copy (CUDA cores)
+    __syncthreads();
+    for (int idx = tid; idx < kTileTok * 16; idx += kTileThreads) {
+      const int i = idx >> 4, p = idx & 15;
+      float f[8];
+      if (i < ntok) unpack8(*reinterpret_cast<const uint4*>(K_rope + (bh * D.s + tok[i]) * kHeadDim + p * 8), f);
+      else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = 0.f;
+      }
+      float4* dst = reinterpret_cast<float4*>(Ks + i * kKsStride + p * 8);
+      dst[0] = make_float4(f[0], f[1], f[2], f[3]);
+      dst[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+    __syncthreads();
+  } else {
+    build_key_tile_tc(&tmA, &tmB, b * D.s + j0 * kChunk, (int)bh * D.r, D.r, R, tok, smem, Ks, &bar_ab, &bar_mma,
+                      &tmem_slot);
+  }
   // warp w: chunks 2w, 2w+1 of the tile; lane: dims 4*lane..+4
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc) {
@@ -49,7 +140,7 @@ k_build_chunks(Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ K_rope, fl
     float4 C = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int u = 0; u < kChunk; ++u) {
-      kv[u] = *reinterpret_cast<const float4*>(Ks + (jl * kChunk + u) * kHeadDim + lane * 4);
+      kv[u] = *reinterpret_cast<const float4*>(Ks + (jl * kChunk + u) * kKsStride + lane * 4);
       C.x += kv[u].x; C.y += kv[u].y; C.z += kv[u].z; C.w += kv[u].w;
     }
     C.x *= 0.125f; C.y *= 0.125f; C.z *= 0.125f; C.w *= 0.125f;       // (1/c) sum, c = 8
@@ -127,7 +218,8 @@ size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base) {
 cudaError_t init_build_attrs() {
   const int sm = (int)keytile_smem_bytes(256);          // the largest rank the ABI accepts
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_build_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, sm))) return e;
+  if ((e = cudaFuncSetAttribute(k_build_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)build_tc_smem_bytes(256)))) return e;
   return cudaFuncSetAttribute(k_build_outliers_window, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
@@ -136,11 +228,27 @@ cudaError_t init_build_attrs() {
 // preceding grid's writes after that wait, so the grid right before a decode must not write them.
 __global__ void k_build_done() {}
 
+static bool encode_map(const DevCtx& ctx, CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                       uint32_t box_inner, uint32_t box_outer) {
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx.encode_tiled);
+  const cuuint64_t gdim[2] = {inner, outer};
+  const cuuint64_t gstride[1] = {inner * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc && enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* K_rope,
-                         const BuildWs& ws, cudaStream_t st, int* launches) {
+                         const BuildWs& ws, cudaStream_t st, int* launches, const DevCtx& ctx) {
   const size_t sm = keytile_smem_bytes(D.r);
+  CUtensorMap tmA, tmB;
+  if (!encode_map(ctx, &tmA, Ly.A, D.r, (uint64_t)D.b * D.s, 64, kTileTok) ||
+      !encode_map(ctx, &tmB, Ly.B, kHeadDim, (uint64_t)D.b * D.hk * D.r, 64, D.r))
+    return cudaErrorInvalidValue;
   dim3 g1((D.n_c + 15) / 16, D.hk, D.b);
-  k_build_chunks<<<g1, kTileThreads, sm, st>>>(D, R, Ly, K_rope, ws.mincos, ws.negm);
+  k_build_chunks<<<g1, kTileThreads, build_tc_smem_bytes(D.r), st>>>(tmA, tmB, D, R, Ly, K_rope, ws.mincos, ws.negm);
   ++*launches;
   if (D.o > 0) {
     k_build_select_outliers<<<dim3(D.hk, D.b), 1024, 0, st>>>(D, ws.negm, Ly.outlier_ids);

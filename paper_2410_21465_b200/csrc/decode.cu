@@ -28,6 +28,7 @@
 #include "append.cuh"
 #include "kernels.h"
 #include "topk.cuh"
+#include "rope.cuh"
 #include "umma.cuh"
 
 namespace skv {
@@ -300,22 +301,24 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   trace(1, 1);
   int* fl = flags + bh * 4;
   if (crank == 0 && tid == 0) st_release_gpu(&fl[0], 1);  // score (incl. a7 window append) complete
-  // ---- lse_hq from the score kernel's per-tile partials: max-reduce, exp-sum-reduce, each in a fixed
-  //      order (lane-strided, then the warp tree): deterministic and independent of the score grid
+  // ---- lse_hq from the score kernel's per-tile partials: one pass, each lane an online (max, sum exp)
+  //      merge of tiles lane, lane+32, ... in order, then a fixed shuffle tree: deterministic and
+  //      independent of the score grid
   if (warp < G) {
     if (warp == 0) trace(1, 13);
     const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * tiles_per_head;
-    float m = -INFINITY;
-    for (int i = lane; i < tiles_per_head; i += 32) m = fmaxf(m, __ldcg(&ph[i].x));
-    m = warp_max(m);
-    if (warp == 0) trace(1, 14);
-    float e = 0.f;
+    float m = -INFINITY, e = 0.f;
     for (int i = lane; i < tiles_per_head; i += 32) {
       const float2 v = __ldcg(&ph[i]);
-      if (v.x > -INFINITY) e += v.y * expf(v.x - m);
+      lse_merge(m, e, v.x, v.y);
     }
-    const float sm = warp_sum(e);
-    if (lane == 0) { lse[warp] = m + logf(sm); hm[warp] = m; }
+    if (warp == 0) trace(1, 14);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), e2 = __shfl_xor_sync(0xffffffffu, e, o);
+      lse_merge(m, e, m2, e2);
+    }
+    if (lane == 0) { lse[warp] = m + logf(e); hm[warp] = m; }
     if (warp == 0) trace(1, 15);
   }
   __syncthreads();
@@ -649,54 +652,6 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
   }
 }
 
-// RoPE (R15) of one token row held as two 32-column blocks x0 = cols [c0, c0+32), x1 = cols [c1, c1+32)
-// of the rebuilt key.  The column sets are chosen so that every rotation pair lies in one thread:
-// halves layout with rot = 128 (Llama): set s holds cols [32s, 32s+32) and their partners +64;
-// rot <= 64 (halves, rot/2 in {8, 16, 32}) or interleaved: set s holds [64s, 64s+64).
-__device__ __forceinline__ void rope_row(float* x0, float* x1, int c0, int c1, int t, const Rope& R) {
-  if (R.interleaved) {
-#pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      float* x = blk ? x1 : x0;
-      const int cb = blk ? c1 : c0;
-#pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        if (cb + e < R.rot) {
-          float sn, cs;
-          rope_sincos(t, __ldg(R.inv_freq + ((cb + e) >> 1)), &sn, &cs);
-          const float a = x[e], b = x[e + 1];
-          x[e] = a * cs - b * sn;
-          x[e + 1] = b * cs + a * sn;
-        }
-      }
-    }
-    return;
-  }
-  const int half = R.rot >> 1;
-  auto rot2 = [&](float& a, float& b, int i) {
-    float sn, cs;
-    rope_sincos(t, __ldg(R.inv_freq + i), &sn, &cs);
-    const float x = a, y = b;
-    a = x * cs - y * sn;
-    b = y * cs + x * sn;
-  };
-  if (half == 64) {                                     // pairs (c0 + e, c0 + 64 + e) = (x0[e], x1[e])
-#pragma unroll
-    for (int e = 0; e < 32; ++e) rot2(x0[e], x1[e], c0 + e);
-  } else if (c0 == 0) {                                 // set 0 holds every rotary dim (rot <= 64)
-    if (half == 32) {
-#pragma unroll
-      for (int e = 0; e < 32; ++e) rot2(x0[e], x1[e], e);
-    } else if (half == 16) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) rot2(x0[e], x0[e + 16], e);
-    } else if (half == 8) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) rot2(x0[e], x0[e + 8], e);
-    }
-  }
-}
-
 template <int G>
 __global__ void __launch_bounds__(256, 2)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -851,8 +806,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     //      warp % 4); the two warps of a row split its 128 columns into RoPE-closed sets (rope_row)
     float x0[32], x1[32];
     const int erow = 32 * (warp & 1) + lane, eset = warp >> 2;
-    const bool hl = !R.interleaved && R.rot > 64;
-    const int c0 = hl ? 32 * eset : 64 * eset, c1 = hl ? 64 + 32 * eset : 64 * eset + 32;
+    int c0, c1;
+    rope_col_sets(R, eset, &c0, &c1);
     const bool epi = (warp & 2) == 0;
     if (epi) {
       mbar_wait(&barMMA, 0);

@@ -127,7 +127,7 @@ cudaError_t launch_score_tc(const Dims& D, const uint16_t* L, const int32_t* oid
 
 // each returns cudaGetLastError() after its launches and adds to *launches
 cudaError_t launch_build(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* K_rope,
-                         const BuildWs& ws, cudaStream_t st, int* launches);
+                         const BuildWs& ws, cudaStream_t st, int* launches, const DevCtx& ctx);
 cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const uint16_t* q,
                           const uint16_t* k_new, const uint16_t* v_new, int step, uint16_t* out,
                           int32_t* sel_ids, uint16_t* dbg_keys, char* ws_base, cudaStream_t st,
