@@ -298,6 +298,10 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   if (tid == 0) { ccnt = 0; info[0] = 255; info[1] = 0; }   // B = 255 unless bins 0..254 reach k
   cluster_arrive_relaxed();                             // #0: this CTA has started (waited on before the
   pdl_wait();                                           //     first DSMEM store; long complete by then)
+  // The sparse grid may launch now: its CTAs stage q and B_h and then poll their selection slots while
+  // this grid selects.  (Not before the wait: that orders this layer's score, and through it the
+  // previous layer's merge -- which re-zeroes the slots -- before any sparse CTA of this call.)
+  pdl_trigger();
   trace(1, 1);
   int* fl = flags + bh * 4;
   if (crank == 0 && tid == 0) st_release_gpu(&fl[0], 1);  // score (incl. a7 window append) complete
@@ -308,9 +312,15 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     if (warp == 0) trace(1, 13);
     const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * tiles_per_head;
     float m = -INFINITY, e = 0.f;
-    for (int i = lane; i < tiles_per_head; i += 32) {
-      const float2 v = __ldcg(&ph[i]);
-      lse_merge(m, e, v.x, v.y);
+    for (int i0 = 0; i0 < tiles_per_head; i0 += 32 * 8) {       // 8 independent loads in flight per lane
+      float2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + lane + 32 * u;
+        v[u] = i < tiles_per_head ? __ldcg(&ph[i]) : make_float2(-INFINITY, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) lse_merge(m, e, v[u].x, v[u].y);
     }
     if (warp == 0) trace(1, 14);
 #pragma unroll
@@ -372,7 +382,6 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   trace(1, 3);
   cluster_sync_all();                                                   // #1 histograms published
   trace(1, 4);
-  pdl_trigger();                                        // sparse CTAs launch and poll their slots
   if (tid < 256) {
     int g = 0;
 #pragma unroll

@@ -5,13 +5,14 @@
 // One UMMA per 16-wide k step: M = 128 landmark rows (A, K-major, SWIZZLE_128B, streamed from HBM
 // by TMA in two 64-column boxes), N = 16 query heads of the GQA group (B, zero-padded, built once
 // per KV head in smem), K = 128 = head_dim, fp32 accumulators in TMEM (8 x 16 columns).  Warp
-// roles (224 threads): warps 0-3 epilogue (TMEM lane quadrant = warp), warp 4 TMA producer,
+// roles (608 threads): 4 epilogue groups of 4 warps (0-3, 7-10, 11-14, 15-18; TMEM lane quadrant =
+// warp % 4) on tiles i % 4, warp 4 TMA producer,
 // warps 5-6 MMA issuers on alternate tiles (measured: one issuing thread is paced at ~70 cycles
 // per tcgen05.mma at any N <= 128, two on different sub-partitions reach ~40, the rate at which
 // the tensor core reads the 4 KB A operand from smem; tools/probe_umma.cu).  The epilogue reads
 // each landmark's G logits with tcgen05.ld, masks outlier chunks (R3), writes the scaled logits
-// and per-(CTA, KV head) softmax partials (max, sum exp) that k_select merges into the exact
-// per-head log-sum-exp.  The first ring fills are issued before griddepcontrol.wait: landmarks
+// and one softmax partial (max, sum exp) per tile and query row, which k_select merges in a fixed
+// order into the exact per-head log-sum-exp.  The first ring fills are issued before griddepcontrol.wait: landmarks
 // are layer state that no decode-step kernel writes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -31,7 +32,8 @@ constexpr int kTcStages = 6;
 constexpr int kTcAcc = 8;                 // TMEM accumulator buffers (16 fp32 columns each)
 constexpr int kTcMaxHeads = 4;            // KV heads a CTA's contiguous tile range may touch
 constexpr int kTcMaxTiles = 64;           // tiles per CTA (outlier bitmap size); the plan never exceeds it
-constexpr int kTcThreads = 352;         // 2 x 4 epilogue warps, 1 TMA producer, 2 MMA issuers
+constexpr int kTcEpiGroups = 4;         // epilogue groups of 4 warps (one per TMEM lane quadrant), alternate tiles
+constexpr int kTcThreads = (4 * kTcEpiGroups + 3) * 32;   // + 1 TMA producer, 2 MMA issuers
 constexpr uint32_t kTileBytes = kSTile * kHeadDim * 2;   // 32 KB: two 16 KB SW128 boxes
 constexpr uint32_t kBBytes = 16 * kHeadDim * 2;          // 4 KB: B operand of one head
 
@@ -79,7 +81,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], acc_full[kTcAcc], acc_empty[kTcAcc];
   __shared__ uint32_t tmem_base;
   __shared__ uint32_t obits[kTcMaxTiles * (kSTile / 32)];
-  __shared__ float2 wpart[2][2][4][16];                        // [group][tile parity][warp][row]
+  __shared__ float2 wpart[kTcEpiGroups][2][4][16];             // [group][tile parity][warp][row]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = D.b * D.hk * tiles_per_head;
   const int t_begin = (int)((long long)blockIdx.x * total / gridDim.x);
@@ -195,7 +197,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
       }
     }
   } else {
-    // ---------------- epilogue: two groups of 4 warps (0-3 and 7-10) on alternate tiles ----------------
+    // ---------------- epilogue: 4 groups of 4 warps (0-3, 7-10, 11-14, 15-18), tile i -> group i % 4 ------
     // Warp w reads TMEM lane quadrant w % 4 (32 landmark rows).  Per tile and query row it writes the
     // logits and ONE softmax partial (max, sum exp) of the tile's 128 landmarks: the four warps' partials
     // meet in smem behind one named barrier of the group and warp quad 0 merges them in a fixed order.
@@ -204,16 +206,16 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     // runs in (batch / head sharding is bit-exact).  Log2 domain; a finite floor stands in for -inf so
     // fully masked rows never produce inf - inf.
     constexpr float kFloor = -1e30f, kLog2e = 1.4426950408889634f, kLn2 = 0.6931471805599453f;
-    const int grp = warp >= 7 ? 1 : 0, quad = warp & 3;
+    const int grp = warp < 4 ? 0 : (warp - 7) / 4 + 1, quad = warp & 3;
     int bh = t_begin / tiles_per_head, tile = t_begin - bh * tiles_per_head;   // advanced incrementally
-    if (grp == 1 && ntile > 1) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
+    for (int k = 0; k < grp && k < ntile; ++k) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
     int cur_bh = -1;
     float* lrow = nullptr;
     float2* prow = nullptr;
     int ncb = 0;
     const int r = 32 * quad + lane;
-    for (int i = grp; i < ntile; i += 2) {
-      const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1, par = (i >> 1) & 1;
+    for (int i = grp; i < ntile; i += kTcEpiGroups) {
+      const int buf = i % kTcAcc, aph = (i / kTcAcc) & 1, par = (i / kTcEpiGroups) & 1;
       if (bh != cur_bh) {
         cur_bh = bh;
         const int b = bh / D.hk, h = bh - b * D.hk;
@@ -242,8 +244,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         const float sm = warp_sum(out ? 0.f : exp2f(x2 - m2));
         if (lane == 0) wpart[grp][par][quad][hq] = make_float2(m2, sm);
       }
-      if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");   // the group's 4 warps
-      else asm volatile("bar.sync 2, 128;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" :: "r"(grp + 1) : "memory");   // the group's 4 warps
       if (quad == 0 && lane < G) {                        // fixed-order merge of the 4 warps (log2 domain)
         float m = kFloor;
 #pragma unroll
@@ -256,7 +257,7 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
         }
         prow[(size_t)lane * tiles_per_head + tile] = m > kFloor ? make_float2(m * kLn2, sm) : make_float2(-INFINITY, 0.f);
       }
-      for (int st2 = 0; st2 < 2; ++st2) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
+      for (int st2 = 0; st2 < kTcEpiGroups; ++st2) { if (++tile == tiles_per_head) { tile = 0; ++bh; } }
     }
     if (warp == 0 && lane == 0) trace_tc_any(trace_buf, 13);     // epilogue loop done
   }
