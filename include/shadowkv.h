@@ -239,12 +239,13 @@ SKV_API size_t shadowkv_factorize_workspace_bytes(const skv_dims *dims);
  * truncated SVD of the pre-RoPE keys with all KV heads concatenated per token (X[t][h*d + j] =
  * K_pre[b][h][t][j], R14), X = U S V^T, split as A = U_r S_r (shared by the heads) and
  * B_h = (V_r^T)[:, h*d:(h+1)*d] -- exactly the factors shadowkv_build_cache / decode_step take.
- * Computed through the D x D Gram matrix (D = h_kv*d): G = X^T X (cuBLAS, bf16 in, fp32 out, tensor
- * cores), eigen-decomposition in fp64 (cuSOLVER dsyevd), A = X V_r (our fp32 CUDA-core kernel).  Each
- * singular vector's largest-magnitude component is made positive (deterministic factors).
- * Dims used: batch, n_kv_heads, head_dim (multiple of 32), ctx_len, rank (multiple of 16,
+ * Computed through the D x D Gram matrix (D = h_kv*d): G = X^T X (our tcgen05 kernel: 128 x 128
+ * blocks, bf16 in, fp32 TMEM accumulation, split over token ranges, partials summed in a fixed order),
+ * eigen-decomposition in fp64 (cuSOLVER dsyevdx, top r), A = X V_r (our tcgen05 kernel; V_r as bf16 hi +
+ * lo planes).  Each singular vector's largest-magnitude component is made positive (deterministic
+ * factors).  Dims used: batch, n_kv_heads, head_dim (must be 128), ctx_len, rank (multiple of 16,
  * 16 <= r <= min(256, s, h_kv*d)); h_kv*d <= 4096.  Prefill-time ("linear cost"), not the
- * decode hot path; creates one cuBLAS and one cuSOLVER handle per process on first use.
+ * decode hot path; creates one cuSOLVER handle per process on first use; needs shadowkv_init.
  * K_pre  device bf16 [b][h_kv][s][d]  (Alg 1 input K)
  * A      device bf16 [b][s][r]        (out)
  * B      device bf16 [b][h_kv][r][d]  (out)

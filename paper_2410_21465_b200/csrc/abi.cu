@@ -323,7 +323,7 @@ static skv_status check_factorize_dims(const skv_dims* d, int* D) {
   if (!d) return fail(SKV_EINVAL, "dims is NULL");
   if (d->batch < 1 || d->n_kv_heads < 1 || d->head_dim < 1 || d->ctx_len < 1)
     return fail(SKV_EINVAL, "batch, n_kv_heads, head_dim and ctx_len must be >= 1");
-  if (d->head_dim % 32) return fail(SKV_EUNSUPPORTED, "head_dim %d not a multiple of 32", d->head_dim);
+  if (d->head_dim != 128) return fail(SKV_EUNSUPPORTED, "head_dim must be 128 (got %d)", d->head_dim);
   const long long Dl = (long long)d->n_kv_heads * d->head_dim;
   if (Dl > 4096) return fail(SKV_EUNSUPPORTED, "n_kv_heads * head_dim = %lld > 4096", Dl);
   if (d->rank < 16 || d->rank > 256 || d->rank % 16)
@@ -351,12 +351,14 @@ skv_status shadowkv_factorize(const skv_dims* dims, const uint16_t* K_pre, uint1
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(SKV_EINVAL, "workspace must be non-NULL and 256-byte aligned");
   NvtxRange nv("shadowkv_factorize");
+  const skv::DevCtx* ctx = need_ctx();
+  if (!ctx) return SKV_ESTATE;
   skv::FactorizeWs ws;
   skv::factorize_ws_bytes(D, dims->rank, &ws, static_cast<char*>(workspace));
   int launches = 0;
   skv::FactorizeResult r = skv::launch_factorize(dims->batch, dims->n_kv_heads, dims->head_dim, dims->ctx_len,
                                                  dims->rank, K_pre, A, B, sigma, ws,
-                                                 static_cast<cudaStream_t>(stream), &launches);
+                                                 static_cast<cudaStream_t>(stream), &launches, *ctx);
   if (r.err != cudaSuccess)
     return fail(SKV_ECUDA, "factorize (%s%s%d): %s", r.what ? r.what : "?", r.unused ? ", lwork " : "", r.unused,
                 cudaGetErrorString(r.err));

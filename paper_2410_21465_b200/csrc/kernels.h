@@ -136,14 +136,12 @@ size_t decode_ws_total_bytes(const Dims& D);   // every sub-batch split's worksp
 cudaError_t launch_rope_probe(const int32_t* pos, int n, const float* inv_freq, int nf, float* out, cudaStream_t st);
 
 // factorize.cu: Alg 1 "A, B <- SVD(K)" through the D x D Gram matrix (NEXT-2)
-constexpr size_t kFactorizeBlasWs = (size_t)32 << 20;   // cuBLAS workspace carved from ours
 struct FactorizeWs {
-  float* G;          // [D][D] fp32 Gram (column-major)
+  float* Gp;         // [splits][D][D] fp32 Gram block partials (row-major, upper block triangle)
   double* Gd;        // [D][D] fp64, overwritten by the eigenvectors
   double* lam;       // [D] eigenvalues, ascending
-  float* W;          // [D][r] top-r right singular vectors
+  uint16_t* WT;      // [2][r][D] bf16: W^T hi and lo planes
   int* info;
-  void* blas_ws;
   double* work;      // dsyevd work
   size_t lwork;      // doubles
 };
@@ -153,7 +151,9 @@ struct FactorizeResult {
   const char* what;  // failing step
 };
 size_t factorize_ws_bytes(int D, int r, FactorizeWs* ws, char* base);
+cudaError_t init_factorize_attrs();
 FactorizeResult launch_factorize(int b, int hk, int d, int s, int r, const uint16_t* K, uint16_t* A, uint16_t* B,
-                                 float* sigma, const FactorizeWs& ws, cudaStream_t st, int* launches);
+                                 float* sigma, const FactorizeWs& ws, cudaStream_t st, int* launches,
+                                 const DevCtx& ctx);
 
 }  // namespace skv

@@ -57,6 +57,7 @@ cudaError_t init_device(int device, const char** what) {
   if ((e = init_decode_attrs())) return done(e, "decode kernel attributes");
   if ((e = init_score_tc_attrs())) return done(e, "score kernel attributes");
   if ((e = init_build_attrs())) return done(e, "build kernel attributes");
+  if ((e = init_factorize_attrs())) return done(e, "factorize kernel attributes");
   g_ctx[device] = c;
   g_ready[device].store(true, std::memory_order_release);
   return done(cudaSuccess, "");
