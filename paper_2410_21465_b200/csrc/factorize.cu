@@ -182,13 +182,14 @@ __global__ void k_take_top(const double* __restrict__ V, const double* __restric
 // 5. A = X . W on the tensor cores: CTA = 128 tokens x r columns, K = D in 64-wide blocks (one head
 //    half each); stage = X box (128 tokens x 64, K-major) + W^T hi and lo boxes (r rows x 64, K-major)
 // ---------------------------------------------------------------------------------------------
-constexpr int kPStages = 3;
+constexpr int kPStages = 3;                      // ring depth (fewer at large r: shared memory)
 __host__ __device__ constexpr uint32_t proj_stage_bytes(int r) { return 16384u + 2u * (uint32_t)r * 128u; }
-size_t project_smem_bytes(int r) { return 1024 + (size_t)kPStages * proj_stage_bytes(r); }
+static int proj_stages(int r) { return (1024 + 3 * (size_t)proj_stage_bytes(r) <= 227 * 1024) ? 3 : 2; }
+size_t project_smem_bytes(int r) { return 1024 + (size_t)proj_stages(r) * proj_stage_bytes(r); }
 
 __global__ void __launch_bounds__(128, 1)
 k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int head0, int hk,
-             int s, int r, uint16_t* __restrict__ A) {
+             int s, int r, int nstage, uint16_t* __restrict__ A) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
   __shared__ __align__(8) uint64_t full[kPStages], empty[kPStages], done;
@@ -198,7 +199,7 @@ k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   const uint32_t stage = proj_stage_bytes(r);
   const uint32_t idesc = umma_idesc_bf16(128, r, false, false);
   if (tid == 0) {
-    for (int i = 0; i < kPStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < nstage; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     mbar_init(&done, 1);
     fence_mbar_init();
     prefetch_tensormap(&tmX);
@@ -211,8 +212,8 @@ k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
   const uint32_t tmem = tmem_slot;
   if (tid == 0) {                                       // TMA producer
     for (int kb = 0; kb < nkb; ++kb) {
-      const int stg = kb % kPStages;
-      if (kb >= kPStages) mbar_wait(&empty[stg], ((kb / kPStages) - 1) & 1);
+      const int stg = kb % nstage;
+      if (kb >= nstage) mbar_wait(&empty[stg], ((kb / nstage) - 1) & 1);
       uint8_t* base = smem + stg * stage;
       mbar_expect_tx(&full[stg], stage);
       tma_load_3d(base, &tmX, (kb & 1) * 64, t0, head0 + (kb >> 1), &full[stg]);
@@ -221,8 +222,8 @@ k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
     }
   } else if (tid == 32) {                               // MMA issuer
     for (int kb = 0; kb < nkb; ++kb) {
-      const int stg = kb % kPStages;
-      mbar_wait(&full[stg], (kb / kPStages) & 1);
+      const int stg = kb % nstage;
+      mbar_wait(&full[stg], (kb / nstage) & 1);
       tc_fence_after();
       const uint32_t x0 = smem_u32(smem + stg * stage), w0 = x0 + 16384, w1 = w0 + r * 128;
 #pragma unroll
@@ -375,7 +376,7 @@ FactorizeResult launch_factorize(int b, int hk, int d, int s, int r, const uint1
                                   sigma ? sigma + (size_t)bi * r : nullptr);
     // 5. A = X W on the tensor cores
     k_project_tc<<<(s + 127) / 128, 128, project_smem_bytes(r), st>>>(tmX, tmW, bi * hk, hk, s, r,
-                                                                      A + (size_t)bi * s * r);
+                                                                      proj_stages(r), A + (size_t)bi * s * r);
     *launches += 4;
     if ((res.err = cudaGetLastError()) != cudaSuccess) { res.what = "kernel launch"; return res; }
   }
