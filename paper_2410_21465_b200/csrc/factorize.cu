@@ -256,8 +256,10 @@ k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CU
 
 cudaError_t init_factorize_attrs() {
   cudaError_t e;
+  size_t proj = 0;
+  for (int r = 16; r <= 256; r += 16) proj = project_smem_bytes(r) > proj ? project_smem_bytes(r) : proj;
   if ((e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem_bytes()))) return e;
-  return cudaFuncSetAttribute(k_project_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)project_smem_bytes(256));
+  return cudaFuncSetAttribute(k_project_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)proj);
 }
 
 namespace {
