@@ -558,6 +558,9 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
 // =============================================================================================
 // a4 + a5 + a6: fused rebuild + host gather + attention over one unit of <= 64 tokens
 // =============================================================================================
+constexpr int kQStride = kHeadDim + 4;       // q rows (floats): conflict-free MMA A fragments
+constexpr int kPStride = kUnitTok + 4;       // logit / probability rows (floats)
+constexpr int kKStride = kHeadDim + 4;       // fp32 key tile rows (floats)
 struct AttnSmem {      // byte offsets from the 1024-aligned base of dynamic smem
   int a, bmat, v, q, pp, p, tok, bytes;
 };
@@ -573,10 +576,11 @@ __host__ __device__ inline AttnSmem attn_smem_layout(int r, int G) {
   s.a = off; off += nkb * 8192 > kUnitTok * kHeadDim * 2 ? nkb * 8192 : kUnitTok * kHeadDim * 2;
   s.bmat = off; off += 2 * r * 128;
   if (off < nkb * 8192 + 8192) off = nkb * 8192 + 8192;
+  if (off < kUnitTok * kKStride * 4) off = kUnitTok * kKStride * 4;           // fp32 key tile (G >= 8) aliases A, B
   s.v = off; off += kUnitTok * kHeadDim * 2;                                // V tile bf16
-  s.q = off; off += G * kHeadDim * 4;                                       // q fp32
+  s.q = off; off += G * kQStride * 4;                                       // q fp32
   s.pp = off; off += 2 * G * kUnitTok * 4;                                  // logit halves (two column sets)
-  s.p = off; off += G * kUnitTok * 4;                                       // logits / probs
+  s.p = off; off += G * kPStride * 4;                                       // logits / probs
   s.tok = off; off += kUnitTok * 4;
   s.bytes = off + 1024;                                                     // + base alignment slack
   return s;
@@ -661,6 +665,56 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
   }
 }
 
+// tf32 operand (round to nearest) for mma.sync
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r; asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x)); return r;
+}
+__device__ __forceinline__ void mma_tf32(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// S[16 query rows][8 tokens of warp w] = Q . K~^T over the 128 dims (rows >= G are zero)
+template <int G>
+__device__ __forceinline__ void qk_tile_mma(const float* qs, const float* Ksm, int warp, int lane, float* c) {
+  const int g = lane >> 2, t = lane & 3;
+  c[0] = c[1] = c[2] = c[3] = 0.f;
+  const float* qa = qs + g * kQStride + t;
+  const float* qb = qs + (g + 8) * kQStride + t;
+  const float* kr = Ksm + (8 * warp + g) * kKStride + t;
+#pragma unroll 4
+  for (int k0 = 0; k0 < kHeadDim; k0 += 8) {
+    const uint32_t a0 = to_tf32(qa[k0]), a2 = to_tf32(qa[k0 + 4]);
+    const uint32_t a1 = g + 8 < G ? to_tf32(qb[k0]) : 0u, a3 = g + 8 < G ? to_tf32(qb[k0 + 4]) : 0u;
+    mma_tf32(c, a0, a1, a2, a3, to_tf32(kr[k0]), to_tf32(kr[k0 + 4]));
+  }
+}
+// O[16 query rows][16 dims of warp w] = P . V over the unit's 64 tokens (rows past ntok contribute 0)
+template <int G>
+__device__ __forceinline__ void pv_tile_mma(const float* P, const uint16_t* Vs, int ntok, int warp, int lane,
+                                            float (*c)[4]) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
+  const float* pa = P + g * kPStride + t;
+  const float* pb = P + (g + 8) * kPStride + t;
+#pragma unroll 2
+  for (int k0 = 0; k0 < kUnitTok; k0 += 8) {
+    const uint32_t a0 = to_tf32(pa[k0]), a2 = to_tf32(pa[k0 + 4]);
+    const uint32_t a1 = g + 8 < G ? to_tf32(pb[k0]) : 0u, a3 = g + 8 < G ? to_tf32(pb[k0 + 4]) : 0u;
+    const int r0 = k0 + t, r1 = k0 + t + 4;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int dim = 16 * warp + 8 * nt + g;
+      const uint32_t b0 = r0 < ntok ? to_tf32(bf2f(Vs[r0 * kHeadDim + dim])) : 0u;
+      const uint32_t b1 = r1 < ntok ? to_tf32(bf2f(Vs[r1 * kHeadDim + dim])) : 0u;
+      mma_tf32(c[nt], a0, a1, a2, a3, b0, b1);
+    }
+  }
+}
+
 template <int G>
 __global__ void __launch_bounds__(256, 2)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -727,7 +781,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   if (rebuild && warp == 0) tmem_alloc<128>(&tmem_base);      // K~ accumulator: 128 lanes x 128 fp32 columns
   // q is a call input: stage it before waiting on the producer kernels
   for (int i = tid; i < G * kHeadDim; i += 256)
-    qs[i] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
+    qs[(i >> 7) * kQStride + (i & 127)] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -850,30 +904,59 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
       }
     }
-    // ---- logits q . k~ (fp32 keys), half a row per thread, combined below in a fixed order
-    if (epi) {
-#pragma unroll 4
-      for (int hq = 0; hq < G; ++hq) {
-        const float* qh = qs + hq * kHeadDim;
-        float a = 0.f, bsum = 0.f;
+    if constexpr (G >= 8) {
+      // ---- logits on the tensor cores (G >= 8 query rows fill an m16 tile): the fp32 post-RoPE keys go
+      //      through smem (over the consumed A / B_h tiles) and S[16][64] = Q[16][128] . K~^T runs as
+      //      mma.sync m16n8k8 TF32 (q is bf16: exact; keys rounded to TF32, 2^-11 relative)
+      float* Ksm = reinterpret_cast<float*>(As);
+      mbar_wait(&barMMA, 0);                             // (every warp: the MMA has read A and B_h)
+      __syncthreads();
+      if (epi) {
+        float* kr = Ksm + erow * kKStride;
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 qa = *reinterpret_cast<const float4*>(qh + c0 + e);
-          const float4 qb = *reinterpret_cast<const float4*>(qh + c1 + e);
-          a = fmaf(x0[e], qa.x, a); a = fmaf(x0[e + 1], qa.y, a); a = fmaf(x0[e + 2], qa.z, a); a = fmaf(x0[e + 3], qa.w, a);
-          bsum = fmaf(x1[e], qb.x, bsum); bsum = fmaf(x1[e + 1], qb.y, bsum);
-          bsum = fmaf(x1[e + 2], qb.z, bsum); bsum = fmaf(x1[e + 3], qb.w, bsum);
+          *reinterpret_cast<float4*>(kr + c0 + e) = make_float4(x0[e], x0[e + 1], x0[e + 2], x0[e + 3]);
+          *reinterpret_cast<float4*>(kr + c1 + e) = make_float4(x1[e], x1[e + 1], x1[e + 2], x1[e + 3]);
         }
-        Pp[(eset * G + hq) * kUnitTok + erow] = a + bsum;
       }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < G * kUnitTok; idx += 256) {
-      const int hq = idx / kUnitTok, row = idx - hq * kUnitTok;
-      // generated low-rank unit: token g = ui*64 + row is seen by query row hq (token i = hq % s_q) iff
-      // g <= step + i (causal, R28)
-      const bool vis = row < ntok && (kind == 0 || ui * kUnitTok + row < stp0 + 1 + hq % D.sq);
-      P[idx] = vis ? (Pp[hq * kUnitTok + row] + Pp[(G + hq) * kUnitTok + row]) * scale : -INFINITY;
+      __syncthreads();
+      float c[4];
+      qk_tile_mma<G>(qs, Ksm, warp, lane, c);
+      const int g = lane >> 2, t = lane & 3, col = 8 * warp + 2 * t;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int hq = g + 8 * (x >> 1), row = col + (x & 1);
+        if (hq < G) {
+          const bool vis = row < ntok && (kind == 0 || ui * kUnitTok + row < stp0 + 1 + hq % D.sq);
+          P[hq * kPStride + row] = vis ? c[x] * scale : -INFINITY;
+        }
+      }
+    } else {
+      // ---- logits q . k~ (fp32 keys), half a row per thread, combined below in a fixed order
+      if (epi) {
+  #pragma unroll 4
+        for (int hq = 0; hq < G; ++hq) {
+          const float* qh = qs + hq * kQStride;
+          float a = 0.f, bsum = 0.f;
+  #pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 qa = *reinterpret_cast<const float4*>(qh + c0 + e);
+            const float4 qb = *reinterpret_cast<const float4*>(qh + c1 + e);
+            a = fmaf(x0[e], qa.x, a); a = fmaf(x0[e + 1], qa.y, a); a = fmaf(x0[e + 2], qa.z, a); a = fmaf(x0[e + 3], qa.w, a);
+            bsum = fmaf(x1[e], qb.x, bsum); bsum = fmaf(x1[e + 1], qb.y, bsum);
+            bsum = fmaf(x1[e + 2], qb.z, bsum); bsum = fmaf(x1[e + 3], qb.w, bsum);
+          }
+          Pp[(eset * G + hq) * kUnitTok + erow] = a + bsum;
+        }
+      }
+      __syncthreads();
+      for (int idx = tid; idx < G * kUnitTok; idx += 256) {
+        const int hq = idx / kUnitTok, row = idx - hq * kUnitTok;
+        // generated low-rank unit: token g = ui*64 + row is seen by query row hq (token i = hq % s_q) iff
+        // g <= step + i (causal, R28)
+        const bool vis = row < ntok && (kind == 0 || ui * kUnitTok + row < stp0 + 1 + hq % D.sq);
+        P[hq * kPStride + row] = vis ? (Pp[hq * kUnitTok + row] + Pp[(G + hq) * kUnitTok + row]) * scale : -INFINITY;
+      }
     }
   } else {
     // ---- outlier or window (R8, R18) unit: exact keys and values from HBM
@@ -923,7 +1006,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int x = 0; x < 16; ++x) pv[x] = 0.f;
 #pragma unroll
       for (int hh = 0; hh < HC; ++hh) {
-        const float4* qp = reinterpret_cast<const float4*>(qs + (h0 + hh) * kHeadDim + tx * 8);
+        const float4* qp = reinterpret_cast<const float4*>(qs + (h0 + hh) * kQStride + tx * 8);
         const float4 q0 = qp[0], q1 = qp[1];
         const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
@@ -940,19 +1023,19 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // window unit: query row hq (token i = hq % s_q) sees new tokens 0..i only (causal, R28)
         const bool vis = row < ntok && (kind == 1 || (kind == 2 && lowrank) ||
                                         ui * kUnitTok + row < T_win - D.sq + 1 + hq % D.sq);
-        P[hq * kUnitTok + row] = vis ? pv[0] * scale : -INFINITY;
+        P[hq * kPStride + row] = vis ? pv[0] * scale : -INFINITY;
       }
     }
   }
   __syncthreads();
   // ---- softmax statistics of this unit (per q head)
   for (int hq = warp; hq < G; hq += 8) {
-    float x0 = P[hq * kUnitTok + lane], x1 = P[hq * kUnitTok + lane + 32];
+    float x0 = P[hq * kPStride + lane], x1 = P[hq * kPStride + lane + 32];
     const float m = warp_max(fmaxf(x0, x1));
     // (a row can be fully masked: a window unit past this query token's causal limit)
     const float e0 = x0 > -INFINITY ? expf(x0 - m) : 0.f, e1 = x1 > -INFINITY ? expf(x1 - m) : 0.f;
-    P[hq * kUnitTok + lane] = e0;
-    P[hq * kUnitTok + lane + 32] = e1;
+    P[hq * kPStride + lane] = e0;
+    P[hq * kPStride + lane + 32] = e1;
     const float l = warp_sum(e0 + e1);
     if (lane == 0) ml[hq] = make_float2(m, l);
   }
@@ -967,27 +1050,48 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     Ly.vc_dir[(size_t)bh * D.n_c + vc_id] = ((vc_gen + 1) << 32) | (unsigned)slot;
   }
   __syncthreads();
-  // ---- PV: thread = (dim pair, head group of 4): bf16x2 value loads, float4 probability loads
-  {
-    const int dp = tid & 63, grp = tid >> 6;
-    const int ntok4 = (ntok + 3) & ~3;                   // P is 0 past ntok; stale V rows are skipped
-    for (int hq = grp; hq < G; hq += 4) {
-      const float* ph = P + hq * kUnitTok;
-      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-      for (int t = 0; t < ntok4; t += 4) {
-        const float4 p4 = *reinterpret_cast<const float4*>(ph + t);
-        const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
+  if constexpr (G >= 8) {
+    // ---- PV on the tensor cores: O[16][128] = P[16][64] . V[64][128], mma.sync m16n8k8 TF32 (values bf16:
+    //      exact; probabilities rounded to TF32); warp w owns dims 16w..16w+15
+    float c[2][4];
+    pv_tile_mma<G>(P, Vs, ntok, warp, lane, c);
+    const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t v2 = t + e < ntok ? *reinterpret_cast<const uint32_t*>(Vs + (t + e) * kHeadDim + 2 * dp) : 0u;
-          float2& a = (e & 1) ? a1 : a0;
-          a.x = fmaf(pp[e], bf_lo(v2), a.x);
-          a.y = fmaf(pp[e], bf_hi(v2), a.y);
+    for (int nt = 0; nt < 2; ++nt) {
+      const int dim = 16 * warp + 8 * nt + 2 * t;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int hq = g + 8 * hh;
+        if (hq < G) {
+          const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+          *reinterpret_cast<float2*>(o_part + row * kHeadDim + dim) = make_float2(c[nt][2 * hh], c[nt][2 * hh + 1]);
+          if (warp == 0 && t == 0) ml_part[row] = ml[hq];
         }
       }
-      const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-      *reinterpret_cast<float2*>(o_part + row * kHeadDim + 2 * dp) = make_float2(a0.x + a1.x, a0.y + a1.y);
-      if (dp == 0) ml_part[row] = ml[hq];
+    }
+  } else {
+    // ---- PV: thread = (dim pair, head group of 4): bf16x2 value loads, float4 probability loads
+    {
+      const int dp = tid & 63, grp = tid >> 6;
+      const int ntok4 = (ntok + 3) & ~3;                   // P is 0 past ntok; stale V rows are skipped
+      for (int hq = grp; hq < G; hq += 4) {
+        const float* ph = P + hq * kPStride;
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        for (int t = 0; t < ntok4; t += 4) {
+          const float4 p4 = *reinterpret_cast<const float4*>(ph + t);
+          const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t v2 = t + e < ntok ? *reinterpret_cast<const uint32_t*>(Vs + (t + e) * kHeadDim + 2 * dp) : 0u;
+            float2& a = (e & 1) ? a1 : a0;
+            a.x = fmaf(pp[e], bf_lo(v2), a.x);
+            a.y = fmaf(pp[e], bf_hi(v2), a.y);
+          }
+        }
+        const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+        *reinterpret_cast<float2*>(o_part + row * kHeadDim + 2 * dp) = make_float2(a0.x + a1.x, a0.y + a1.y);
+        if (dp == 0) ml_part[row] = ml[hq];
+      }
     }
   }
   if (vc_id >= 0 && Ly.vc_dir) bulk_wait_read();         // the cache write-back has read its smem
