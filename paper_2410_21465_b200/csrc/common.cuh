@@ -99,6 +99,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
                " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive_plain(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
@@ -147,6 +154,24 @@ __device__ __forceinline__ void load_row(const float* src, float* x) {
   }
 }
 
+// 8-byte {value, flag} pairs (the LL-protocol idiom), accessed as ONE 64-bit relaxed.gpu scalar (single-copy
+// atomic): a reader that sees the flag sees the value written with it -- no fence on the writer's side (a
+// release on an SM with host reads in flight waits for all of them, tools/probe_fence.cu)
+__device__ __forceinline__ void st_tagged(uint2* p, float v, unsigned tag) {
+  const unsigned long long x = ((unsigned long long)tag << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ uint2 ld_tagged(const uint2* p) {
+  unsigned long long x;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+  return make_uint2((unsigned)x, (unsigned)(x >> 32));
+}
+__device__ __forceinline__ unsigned ld_volatile_u32(const int* p) {
+  unsigned r;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+
 // programmatic dependent launch (PDL)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -186,6 +211,12 @@ __device__ __forceinline__ int ld_dsmem_i32(uint32_t a) {
 }
 __device__ __forceinline__ void st_dsmem_i32(uint32_t a, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
+// 16 B store into a peer CTA's smem that completes 16 bytes of tx on the peer's mbarrier (both
+// shared::cluster addresses from dsmem_addr)
+__device__ __forceinline__ void st_async_v4(uint32_t a, int4 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.s32 [%0], {%1, %2, %3, %4}, [%5];"
+               :: "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(remote_bar) : "memory");
 }
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t a) {
   float v; asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v;

@@ -16,7 +16,7 @@
 //                     their keys from rank-r rows.  The host fetch is in flight from the kernel's first
 //                     microseconds, so rebuild and attention math hide under it (the paper's multi-stream
 //                     overlap of P:40 / P:460, inside one grid).
-//   k_relay, k_merge  the per-unit partials of each (b, q row) are combined by log-sum-exp into the bf16
+//   k_merge           the per-unit partials of each (b, q row) are combined by log-sum-exp into the bf16
 //                     output; the merge also closes the value cache's generation and re-zeroes the slots.
 // Kernels after the first are launched with programmatic dependent launch (PDL).
 #include <cstdlib>
@@ -276,13 +276,24 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   extern __shared__ __align__(16) float zdyn[];
   __shared__ TopKSmem<NT> tk;
   __shared__ float lse[G], hm[G];
-  __shared__ int hist[256], ghist[256], below[kSelCL], info[4];
-  __shared__ int allhist[kSelCL * 256];                 // every rank's histogram (pushed before #1)
-  __shared__ int cidx[kSelCandLocal], ccnt;
-  __shared__ uint32_t ckey[kSelCandLocal];
-  __shared__ int aidx[kSelCandLocal];
-  __shared__ uint32_t akey[kSelCandLocal];
-  __shared__ int tks[kSelCandLocal], tkf[kSelCandLocal];
+  __shared__ __align__(16) int hist[256];
+  __shared__ int ghist[256], below[kSelCL], info[4];
+  __shared__ __align__(16) int allhist[kSelCL * 256];   // every rank's histogram (st.async pushes -> hbar)
+  __shared__ __align__(8) uint64_t hbar;
+  __shared__ int wdef[NW];
+  __shared__ int cidx[kSelCandPush], ccnt;             // this rank's threshold-bucket candidates
+  __shared__ uint32_t ckey[kSelCandPush];
+  // every rank's {count, 0, 0, 0} + (index, key) pairs, pushed by st.async (completing bytes on cbar)
+  __shared__ __align__(16) int4 cand_in[kSelCL][kSelCandPush / 2 + 1];
+  __shared__ __align__(8) uint64_t cbar;
+  // per-warp bucket histograms (z pass .. publish pass), then the gathered candidates (after #2)
+  static_assert(NW * 256 == 4 * kSelCandLocal, "scratch union");
+  __shared__ __align__(16) int scratch[4 * kSelCandLocal];
+  int (*whist)[256] = reinterpret_cast<int (*)[256]>(scratch);
+  int* aidx = scratch;
+  uint32_t* akey = reinterpret_cast<uint32_t*>(scratch + kSelCandLocal);
+  int* tks = scratch + 2 * kSelCandLocal;
+  int* tkf = scratch + 3 * kSelCandLocal;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t crank = cluster_ctarank();
   const size_t bh = blockIdx.x / kSelCL;
@@ -294,41 +305,75 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   const float* lb = logits + ((size_t)b * D.hq + (size_t)h * G) * n + (size_t)lo * G;   // [n][G]
   int32_t* out = sel + bh * k;
   trace(1, 0);
-  for (int i = tid; i < 256; i += NT) hist[i] = 0;
-  if (tid == 0) { ccnt = 0; info[0] = 255; info[1] = 0; }   // B = 255 unless bins 0..254 reach k
+  for (int i = tid; i < NW * 256; i += NT) (&whist[0][0])[i] = 0;
+  if (tid == 0) {
+    ccnt = 0; info[0] = 255; info[1] = 0;               // B = 255 unless bins 0..254 reach k
+    // every rank pushes its 1 KB histogram into allhist[rank][.] of every rank with st.async, which
+    // completes bytes on this barrier: no cluster barrier between the histograms and their use
+    mbar_init(&hbar, 1);
+    mbar_init(&cbar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&hbar, kSelCL * 256 * 4);
+    mbar_expect_tx(&cbar, kSelCL * (kSelCandPush / 2 + 1) * 16);
+  }
   cluster_arrive_relaxed();                             // #0: this CTA has started (waited on before the
-  pdl_wait();                                           //     first DSMEM store; long complete by then)
+                                                        //     first DSMEM store; long complete by then)
   // The sparse grid may launch now: its CTAs stage q and B_h and then poll their selection slots while
-  // this grid selects.  (Not before the wait: that orders this layer's score, and through it the
-  // previous layer's merge -- which re-zeroes the slots -- before any sparse CTA of this call.)
+  // this grid waits for the scores and selects.  Safe before our griddepcontrol.wait: the score grid
+  // triggers this grid only after ITS wait, i.e. after the previous layer's merge (which re-zeroes the
+  // slots and flags) has completed, so no sparse CTA of this call can see a stale slot.
   pdl_trigger();
+  pdl_wait();
   trace(1, 1);
   int* fl = flags + bh * 4;
-  if (crank == 0 && tid == 0) st_release_gpu(&fl[0], 1);  // score (incl. a7 window append) complete
-  // ---- lse_hq from the score kernel's per-tile partials: one pass, each lane an online (max, sum exp)
-  //      merge of tiles lane, lane+32, ... in order, then a fixed shuffle tree: deterministic and
-  //      independent of the score grid
+  // score (incl. a7 window append) complete; the release store is left to the last warp, which has no
+  // lse work (warps < G are on the critical path)
+  if (crank == 0 && tid == NT - 32) st_release_gpu(&fl[0], 1);
+  // ---- lse_hq from the score kernel's per-tile partials (warps < G) and the first z-pass logits: both
+  //      load batches are issued before either is used (their L2 latencies overlap).  Each lane merges
+  //      its tiles lane, lane+32, ... in batches of 8 (batch max, then one sum of 8 independent exps),
+  //      then a fixed warp tree (max, then rescaled sum): deterministic and independent of the score grid
+  constexpr int U = G >= 8 ? 1 : 4;
+  float lg[U][G];
+  auto load_lg = [&](int j0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * NT + tid;
+#pragma unroll
+      for (int hq = 0; hq < G; ++hq) lg[u][hq] = -INFINITY;
+      if (j < len) load_row<G>(lb + (size_t)j * G, lg[u]);
+    }
+  };
+  const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + (warp < G ? warp : 0)) * tiles_per_head;
+  float2 pv[8];
+  auto load_part = [&](int i0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + lane + 32 * u;
+      pv[u] = i < tiles_per_head ? __ldcg(&ph[i]) : make_float2(-INFINITY, 0.f);
+    }
+  };
+  if (warp < G) load_part(0);
+  load_lg(0);
   if (warp < G) {
     if (warp == 0) trace(1, 13);
-    const float2* ph = part + ((size_t)b * D.hq + (size_t)h * G + warp) * tiles_per_head;
     float m = -INFINITY, e = 0.f;
-    for (int i0 = 0; i0 < tiles_per_head; i0 += 32 * 8) {       // 8 independent loads in flight per lane
-      float2 v[8];
+    for (int i0 = 0; i0 < tiles_per_head; i0 += 32 * 8) {
+      if (i0 > 0) load_part(i0);
+      float mb = pv[0].x;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + lane + 32 * u;
-        v[u] = i < tiles_per_head ? __ldcg(&ph[i]) : make_float2(-INFINITY, 0.f);
+      for (int u = 1; u < 8; ++u) mb = fmaxf(mb, pv[u].x);
+      if (mb > -INFINITY) {
+        float sb = 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sb += pv[u].y * expf(pv[u].x - mb);
+        lse_merge(m, e, mb, sb);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) lse_merge(m, e, v[u].x, v[u].y);
     }
     if (warp == 0) trace(1, 14);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), e2 = __shfl_xor_sync(0xffffffffu, e, o);
-      lse_merge(m, e, m2, e2);
-    }
-    if (lane == 0) { lse[warp] = m + logf(e); hm[warp] = m; }
+    const float M = warp_max(m);
+    const float E = warp_sum(m > -INFINITY ? e * expf(m - M) : 0.f);
+    if (lane == 0) { lse[warp] = M > -INFINITY ? M + logf(E) : -INFINITY; hm[warp] = M; }
     if (warp == 0) trace(1, 15);
   }
   __syncthreads();
@@ -339,17 +384,12 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   const int sq = D.sq;
   if (sq > 1) zmax += logf((float)sq);    // z = log sum_i S_i <= max_i log S_i + log s_q (an upper bound)
   trace(1, 2);
-  // ---- z = max_g (l - lse) on the slice (R4, R5) + bucket histogram
-  constexpr int U = G >= 8 ? 1 : 4;
+  // ---- z = max_g (l - lse) on the slice (R4, R5) + bucket histograms, one per warp: the
+  //      publish pass below walks each warp's elements in the same order, so the definite chunks' slot
+  //      positions follow from the per-warp counts without a block-wide scan
+  int* wh = whist[warp];
   for (int j0 = 0; j0 < len; j0 += U * NT) {
-    float lg[U][G];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * NT + tid;
-#pragma unroll
-      for (int hq = 0; hq < G; ++hq) lg[u][hq] = -INFINITY;
-      if (j < len) load_row<G>(lb + (size_t)j * G, lg[u]);
-    }
+    if (j0 > 0) load_lg(j0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * NT + tid;
@@ -366,21 +406,30 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
         // the catch-all bucket 255 is never counted: if bins 0..254 hold fewer than k, B stays 255
         // and the exact radix fallback runs
         const int bk = zz > -INFINITY ? zbucket(zz, zmax) : 255;
-        if (bk != 255) atomicAdd(&hist[bk], 1);
+        if (bk != 255) atomicAdd(&wh[bk], 1);
       }
     }
   }
-  __syncthreads();                                                      // local histogram complete
-  // push this rank's histogram into allhist[crank][.] of every rank (the release-arrive of barrier #1
-  // orders these remote stores), so that after the barrier all histograms are local reads
-  cluster_wait_acquire();                               // #0: every CTA of the cluster has started
+  __syncthreads();                                                      // per-warp histograms complete
   if (tid < 256) {
-    const int v = hist[tid];
+    int s = 0;
 #pragma unroll
-    for (int r = 0; r < kSelCL; ++r) st_dsmem_i32(dsmem_addr(&allhist[crank * 256 + tid], r), v);
+    for (int w = 0; w < NW; ++w) s += whist[w][tid];
+    hist[tid] = s;
   }
   trace(1, 3);
-  cluster_sync_all();                                                   // #1 histograms published
+  // push this rank's histogram into allhist[crank][.] of every rank (the release-arrive of barrier #1
+  // orders these remote stores), so that after the barrier all histograms are local reads
+  __syncthreads();                                      // hist[] complete
+  cluster_wait_acquire();                               // #0: every CTA of the cluster has started (its
+                                                        //     hbar is initialised)
+  if (tid < 64) {
+    const int4 v = *reinterpret_cast<const int4*>(&hist[4 * tid]);
+#pragma unroll
+    for (int r = 0; r < kSelCL; ++r)
+      st_async_v4(dsmem_addr(&allhist[crank * 256 + 4 * tid], r), v, dsmem_addr(&hbar, r));
+  }
+  mbar_wait(&hbar, 0);                                                  // all kSelCL histograms landed
   trace(1, 4);
   if (tid < 256) {
     int g = 0;
@@ -409,63 +458,82 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   __syncthreads();
   trace(1, 10);
   const int B = info[0], need = info[1];
-  if (warp < kSelCL) {                                  // below[r]: rank r's histogram mass above B
-    int sb = 0;
-    for (int bin = lane; bin < B; bin += 32) sb += allhist[warp * 256 + bin];
-    sb = __reduce_add_sync(0xffffffffu, sb);
-    if (lane == 0) below[warp] = sb;
-  }
   // The selection is published into k slots (chunk id + 1; 0 = not yet) before it is complete:
   // attention is a sum over the selected set, so the chunks strictly above the threshold bucket
   // ("definite") are written to slots [0, k - need) as soon as B is known, and the `need` winners of
-  // bucket B fill [k - need, k) once ranked.  Positions are deterministic (rank prefix, then index
-  // order inside the rank), so the definite part is even ascending.  Each sparse-attention unit
-  // polls its own 8 slots.
+  // bucket B fill [k - need, k) once ranked.  Positions are deterministic: rank prefix (every rank's
+  // histogram mass above B), then the warps of this rank in order, then each warp's elements in z-pass
+  // order.  Each sparse-attention unit polls its own 8 slots.
   int32_t* slots = sel + bh * k;
   const bool prepub = !(B == 255 || n_per > 16384 || force_fb == 1);  // else: radix fallback publishes all k
   bool fallback = !prepub;
-  const int per = (len + NT - 1) / NT;                  // this thread's contiguous run [ja, jb)
-  const int ja = min(len, tid * per), jb = min(len, ja + per);
-  int ndef = 0;
-  if (prepub) {                                         // one pass: candidates of B, definite count
-    for (int i = 0; i < per; ++i) {                     // warp-uniform trip count (ballots inside)
-      const int j = ja + i;
-      float zz = -INFINITY;
-      int bk = 256;
-      if (j < jb) { zz = z[j]; if (zz > -INFINITY) bk = zbucket(zz, zmax); }
-      ndef += bk < B;
-      const unsigned cb = __ballot_sync(0xffffffffu, bk == B);
-      if (cb) {                                         // warp-aggregated slot reservation
-        int base = 0;
-        if (lane == __ffs(cb) - 1) base = atomicAdd(&ccnt, __popc(cb));
-        base = __shfl_sync(0xffffffffu, base, __ffs(cb) - 1);
-        const int pos = base + __popc(cb & ((1u << lane) - 1u));
-        if (bk == B && pos < kSelCandLocal) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
+  // below[r]: rank r's histogram mass above B (one warp per rank), then this warp's definite count;
+  // 8 independent, bank-conflict-free loads per lane
+  auto mass_below = [&](const int* hrow) {
+    int sacc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { const int bin = lane + 32 * i; sacc += bin < B ? hrow[bin] : 0; }
+    return __reduce_add_sync(0xffffffffu, sacc);
+  };
+  if (warp < kSelCL) { const int sb = mass_below(&allhist[warp * 256]); if (lane == 0) below[warp] = sb; }
+  if (prepub) { const int myd = mass_below(whist[warp]); if (lane == 0) wdef[warp] = myd; }
+  __syncthreads();
+  if (prepub) {
+    int base = 0;                                       // ranks below, then warps below in this rank
+    for (int r = 0; r < (int)crank; ++r) base += below[r];
+    for (int w = 0; w < warp; ++w) base += wdef[w];
+    // one pass over the warp's z (in z-pass order): definite -> slot, bucket B -> candidate list
+    for (int j0 = 0; j0 < len; j0 += U * NT) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u * NT + tid;
+        float zz = -INFINITY;
+        int bk = 256;
+        if (j < len) { zz = z[j]; if (zz > -INFINITY) bk = zbucket(zz, zmax); }
+        const unsigned db = __ballot_sync(0xffffffffu, bk < B);
+        if (bk < B) st_relaxed_gpu(&slots[base + __popc(db & ((1u << lane) - 1u))], lo + j + 1);
+        base += __popc(db);
+        const unsigned cb = __ballot_sync(0xffffffffu, bk == B);
+        if (cb) {                                       // warp-aggregated candidate reservation
+          int cbase = 0;
+          if (lane == __ffs(cb) - 1) cbase = atomicAdd(&ccnt, __popc(cb));
+          cbase = __shfl_sync(0xffffffffu, cbase, __ffs(cb) - 1);
+          const int pos = cbase + __popc(cb & ((1u << lane) - 1u));
+          if (bk == B && pos < kSelCandPush) { cidx[pos] = lo + j; ckey[pos] = f2key(zz); }
+        }
       }
     }
   }
-  int dtot;
-  const int dex = block_exclusive_scan<NT>(ndef, tk, &dtot);          // (synchronises the CTA)
+  __syncthreads();                                      // candidates and ccnt complete
   trace(1, 11);
-  // #2 (candidates published in smem): arrive now, wait after the slot stores below
-  cluster_arrive_release();
-  if (ndef) {
-    int base = dex;
-    for (int r = 0; r < (int)crank; ++r) base += below[r];
-    for (int j = ja; j < jb; ++j) {
-      const float zz = z[j];
-      if (zz > -INFINITY && zbucket(zz, zmax) < B) st_relaxed_gpu(&slots[base++], lo + j + 1);
+  // Candidate exchange: this rank's count and its (index, key) pairs go to every rank by st.async,
+  // completing bytes on the receiver's cbar (armed at kernel start).  No cluster barrier: its release
+  // would wait until the co-resident sparse CTAs' host reads -- started by the slots just published --
+  // have landed (a release on an SM waits for all of its outstanding reads, tools/probe_fence.cu).
+  {
+    const int mycnt = ccnt;
+    if (tid <= kSelCandPush / 2) {
+      int4 v = make_int4(mycnt, 0, 0, 0);
+      if (tid > 0) {
+        const int p0 = 2 * (tid - 1), p1 = p0 + 1;
+        v = make_int4(p0 < mycnt ? cidx[p0] : 0, p0 < mycnt ? (int)ckey[p0] : 0,
+                      p1 < mycnt ? cidx[p1] : 0, p1 < mycnt ? (int)ckey[p1] : 0);
+      }
+#pragma unroll
+      for (int r = 0; r < kSelCL; ++r) st_async_v4(dsmem_addr(&cand_in[crank][tid], r), v, dsmem_addr(&cbar, r));
     }
   }
+  const int per = (len + NT - 1) / NT;                  // this thread's contiguous run [ja, jb) (sel_user)
+  const int ja = min(len, tid * per), jb = min(len, ja + per);
   trace(1, 5);
-  cluster_wait_acquire();                                               // #2 candidates visible
+  mbar_wait(&cbar, 0);                                  // every rank's candidates are in cand_in
   trace(1, 6);
   int rc[kSelCL], total = 0, cmax = 0, off = 0;
 #pragma unroll
-  for (int r = 0; r < kSelCL; ++r) rc[r] = fallback ? 0 : ld_dsmem_i32(dsmem_addr(&ccnt, r));
+  for (int r = 0; r < kSelCL; ++r) rc[r] = fallback ? 0 : cand_in[r][0].x;
 #pragma unroll
   for (int r = 0; r < kSelCL; ++r) { total += rc[r]; cmax = max(cmax, rc[r]); off += r < (int)crank ? rc[r] : 0; }
-  fallback = fallback || cmax > kSelCandLocal || total > kSelCandLocal || force_fb == 2;
+  fallback = fallback || cmax > kSelCandPush || total > kSelCandLocal || force_fb == 2;
   if (!fallback) {
     // all ranks' candidates -> local smem; each CTA ranks its own (larger z first, ties -> lower
     // index, R12): rank < need is taken, and the rank is its slot offset in [k - need, k)
@@ -474,11 +542,11 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
 #pragma unroll
       for (int rr = 0; rr < kSelCL; ++rr) { const bool past = t >= base + rc[rr] && rr == r; base += past ? rc[rr] : 0; r += past; }
       const int c = t - base;
-      aidx[t] = ld_dsmem_i32(dsmem_addr(&cidx[c], r));
-      akey[t] = (uint32_t)ld_dsmem_i32(dsmem_addr(&ckey[c], r));
+      const int4 pr = cand_in[r][1 + (c >> 1)];
+      aidx[t] = (c & 1) ? pr.z : pr.x;
+      akey[t] = (uint32_t)((c & 1) ? pr.w : pr.y);
     }
     __syncthreads();
-    cluster_arrive_relaxed();                            // #3: this CTA's DSMEM reads are done
     trace(1, 8);
     for (int t = off + tid; t < off + rc[crank]; t += NT) {
       const uint32_t u = akey[t];
@@ -527,7 +595,6 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
       }
     }
     trace(1, 12);
-    cluster_wait_acquire();                              // #3: peers done reading this CTA's smem
   } else {                   // pathological score distribution: exact radix select on one CTA
     float* zg = zws + bh * n;
     if (ZSMEM)
@@ -589,28 +656,51 @@ constexpr uint32_t kIdescRebuild = umma_idesc_bf16(128, 128, false, true);   // 
 
 // a6 combine: out_hq = sum_s w_s o_s with w_s = exp(m_s - M) / sum_s' l_s' exp(m_s' - M) over the
 // per-unit partials (m_s, l_s, o_s) of one q head (split-KV log-sum-exp merge, fixed order).  A grid
-// of its own (one CTA per (b, hq), thread = dim) behind the relay grid: the kernel boundary orders
-// the partials before it (no fence in the sparse units, whose __threadfence stalls for tens of
-// microseconds while PCIe reads are in flight), and its griddepcontrol.wait is released ~0.8 us
-// after the sparse grid drains.  The first CTA of each (b, h) re-zeroes that head's slots and flags.
+// of its own (one CTA per (b, hq), thread = dim), launched by PDL while the sparse grid still runs.
+// It does not wait on that grid: the units write their partials as 8-byte {value, tag} pairs
+// (tag = this row's epoch + 1) and the merge polls for the tags.  A grid boundary would release it
+// only ~4 us after the last host read, and a per-unit release fence would stall on the SM's other
+// host reads (tools/probe_fence.cu).  Afterwards it bumps the row's epoch; the first CTA of each (b, h)
+// re-zeroes that head's slots and flags (every unit of the head is past them: it wrote its partials).
 template <int G>
 __global__ void __launch_bounds__(kHeadDim)
-k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_part, int n_split,
-        int32_t* __restrict__ sel, int* __restrict__ flags, uint16_t* __restrict__ out, int late_trigger,
-        unsigned long long* __restrict__ vc_stats) {
+k_merge(Dims D, const uint2* __restrict__ o_part, const uint2* __restrict__ ml_part, int* __restrict__ epochs,
+        int n_split, int32_t* __restrict__ sel, int* __restrict__ flags, uint16_t* __restrict__ out,
+        int late_trigger, unsigned long long* __restrict__ vc_stats) {
   TRACE_INIT;
   extern __shared__ __align__(16) float2 mls[];          // [n_split]
   const int row = blockIdx.x, d = threadIdx.x;            // row = b * hq + hq
   if (!late_trigger) pdl_trigger();
-  pdl_wait();
+  // (no griddepcontrol.wait: the previous merge of this row completed before this call's units read
+  //  the epoch -- they start after the score grid's wait -- and this call's partials carry the tag)
+  const unsigned tag = ld_volatile_u32(&epochs[row]) + 1u;
   trace(3, 0);
-  const float2* mr = ml_part + (size_t)row * n_split;
-  const float* orow = o_part + (size_t)row * n_split * kHeadDim + d;
-  for (int i = d; i < n_split; i += kHeadDim) mls[i] = __ldcg(&mr[i]);
+  const uint2* mr = ml_part + (size_t)row * n_split * 2;
+  const uint2* orow = o_part + (size_t)row * n_split * kHeadDim + d;
+  for (int i = d; i < n_split; i += kHeadDim) {           // (m, l) of every unit, polled with back-off
+    uint2 m2, l2;
+    for (;;) {
+      m2 = ld_tagged(mr + 2 * i); l2 = ld_tagged(mr + 2 * i + 1);
+      if (m2.y == tag && l2.y == tag) break;
+      __nanosleep(128);
+    }
+    mls[i] = make_float2(__uint_as_float(m2.x), __uint_as_float(l2.x));
+  }
+  __syncthreads();                                        // every unit's (m, l) has landed
+  trace(3, 2);
   constexpr int kBatch = 64;                              // partial loads in flight per thread
   float v[kBatch];
+  auto load_o = [&](int s0) {                             // (a value may trail its unit's (m, l): re-poll)
+    uint2 t[kBatch];
 #pragma unroll
-  for (int u = 0; u < kBatch; ++u) v[u] = u < n_split ? __ldcg(orow + (size_t)u * kHeadDim) : 0.f;
+    for (int u = 0; u < kBatch; ++u) t[u] = s0 + u < n_split ? ld_tagged(orow + (size_t)(s0 + u) * kHeadDim) : make_uint2(0u, tag);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      while (t[u].y != tag) { __nanosleep(32); t[u] = ld_tagged(orow + (size_t)(s0 + u) * kHeadDim); }
+      v[u] = __uint_as_float(t[u].x);
+    }
+  };
+  load_o(0);
   // weights, computed once per CTA: M = max_s m_s; w_s = exp(m_s - M); L = sum_s l_s w_s
   __shared__ float red[kHeadDim / 32];
   float* w = reinterpret_cast<float*>(mls + n_split);     // [n_split]
@@ -640,10 +730,7 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
   for (int i = 0; i < kHeadDim / 32; ++i) L += red[i];    // fixed order: deterministic
   float acc = 0.f;
   for (int s0 = 0; s0 < n_split; s0 += kBatch) {
-    if (s0 > 0) {
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) v[u] = s0 + u < n_split ? __ldcg(orow + (size_t)(s0 + u) * kHeadDim) : 0.f;
-    }
+    if (s0 > 0) load_o(s0);
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
       if (s0 + u < n_split) acc = fmaf(w[s0 + u], v[u], acc);
@@ -651,6 +738,8 @@ k_merge(Dims D, const float* __restrict__ o_part, const float2* __restrict__ ml_
   if (late_trigger) pdl_trigger();                        // the next grid's prefetch after our loads
   out[(size_t)row * kHeadDim + d] = f2bf(acc / L);
   trace(3, 1);
+  __syncthreads();                                        // every thread has read its partials
+  if (d == 0) epochs[row] = (int)tag;                     // (the next call reads it after this grid completes)
   const int hq = row % D.hq;
   if (hq % G == 0) {                                      // one CTA per (b, h): reset for the next call
     const int bh = (row / D.hq) * D.hk + hq / G;
@@ -691,17 +780,22 @@ __device__ __forceinline__ void qk_tile_mma(const float* qs, const float* Ksm, i
     mma_tf32(c, a0, a1, a2, a3, to_tf32(kr[k0]), to_tf32(kr[k0 + 4]));
   }
 }
-// O[16 query rows][16 dims of warp w] = P . V over the unit's 64 tokens (rows past ntok contribute 0)
+// O[16 query rows][16 dims of warp w] = P . V over the unit's 64 tokens (rows past ntok contribute 0); k step
+// k0 = chunk k0/8: with per_chunk, each chunk's values are waited for (barVc[chunk]) just before its step,
+// otherwise all values (barVc[0]) before the first
 template <int G>
 __device__ __forceinline__ void pv_tile_mma(const float* P, const uint16_t* Vs, int ntok, int warp, int lane,
-                                            float (*c)[4]) {
+                                            float (*c)[4], uint64_t* barVc, bool per_chunk) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
   const float* pa = P + g * kPStride + t;
   const float* pb = P + (g + 8) * kPStride + t;
+  if (!per_chunk) mbar_wait(&barVc[0], 0);
 #pragma unroll 2
   for (int k0 = 0; k0 < kUnitTok; k0 += 8) {
+    if (k0 >= ntok) break;
+    if (per_chunk) mbar_wait(&barVc[k0 >> 3], 0);
     const uint32_t a0 = to_tf32(pa[k0]), a2 = to_tf32(pa[k0 + 4]);
     const uint32_t a1 = g + 8 < G ? to_tf32(pb[k0]) : 0u, a3 = g + 8 < G ? to_tf32(pb[k0 + 4]) : 0u;
     const int r0 = k0 + t, r1 = k0 + t + 4;
@@ -720,7 +814,8 @@ __global__ void __launch_bounds__(256, 2)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmG, Dims D, Rope R, Layer Ly, const uint16_t* __restrict__ q,
               int32_t* __restrict__ sel, int* __restrict__ flags, int step,
-              float* __restrict__ o_part, float2* __restrict__ ml_part, int n_sel_u, int n_out_u, int n_win_u,
+              uint2* __restrict__ o_part, uint2* __restrict__ ml_part, const int* __restrict__ epochs, int n_sel_u,
+              int n_out_u, int n_win_u,
               int n_gen_u, int n_split, float scale, uint16_t* __restrict__ dbg, int early_next) {
   TRACE_INIT;
   extern __shared__ uint8_t smem_raw[];
@@ -733,9 +828,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   float* Pp = reinterpret_cast<float*>(smem + lay.pp);         // [2][G][64]
   float* P = reinterpret_cast<float*>(smem + lay.p);           // [G][64]
   int* tok = reinterpret_cast<int*>(smem + lay.tok);
-  __shared__ __align__(8) uint64_t barAB, barV, barMMA;
+  // barVc[c]: values of chunk c of a selected-chunk unit (one bulk copy each, so the PV can start on
+  // the chunks that have landed); other unit kinds use barVc[0] for their single value copy
+  __shared__ __align__(8) uint64_t barAB, barVc[8], barMMA;
   __shared__ uint32_t tmem_base;
   __shared__ float2 ml[G];
+  __shared__ unsigned tagv[G];                                 // this call's partial tag per q row
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane & 15;
   const int BH = D.b * D.hk;
   const int stp0 = cur_step(D, step);
@@ -762,8 +860,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   if (kind == 3 && ui * kUnitTok >= n_gen) {                    // generated unit past the live tokens
     for (int hq = tid >> 7; hq < G; hq += 2) {
       const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-      o_part[row * kHeadDim + (tid & 127)] = 0.f;
-      if ((tid & 127) == 0) ml_part[row] = make_float2(-INFINITY, 0.f);
+      const unsigned tg = ld_volatile_u32(&epochs[(size_t)b * D.hq + (size_t)h * G + hq]) + 1u;
+      st_tagged(o_part + row * kHeadDim + (tid & 127), 0.f, tg);
+      if ((tid & 127) == 0) { st_tagged(ml_part + 2 * row, -INFINITY, tg); st_tagged(ml_part + 2 * row + 1, 0.f, tg); }
     }
     return;
   }
@@ -772,13 +871,15 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const bool rebuild = kind == 0 || kind == 3;
   trace(2, 0);
   if (tid == 0) {   // selected-chunk units: one arrival per chunk-issuing thread
-    mbar_init(&barAB, kind == 0 ? nch : 1); mbar_init(&barV, kind == 0 ? nch : 1); mbar_init(&barMMA, 1);
+    mbar_init(&barAB, kind == 0 ? nch : 1); mbar_init(&barMMA, 1);
+    for (int c = 0; c < 8; ++c) mbar_init(&barVc[c], 1);
     fence_mbar_init();
     if (rebuild)                                          // B_h's bytes, before any arrival can complete the phase
       asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;"
                    :: "r"(smem_u32(&barAB)), "r"((uint32_t)(2 * D.r * 128)) : "memory");
   }
   if (rebuild && warp == 0) tmem_alloc<128>(&tmem_base);      // K~ accumulator: 128 lanes x 128 fp32 columns
+  if (tid < G) tagv[tid] = ld_volatile_u32(&epochs[(size_t)b * D.hq + (size_t)h * G + tid]) + 1u;
   // q is a call input: stage it before waiting on the producer kernels
   for (int i = tid; i < G * kHeadDim; i += 256)
     qs[(i >> 7) * kQStride + (i & 127)] = bf2f(q[((size_t)b * D.hq + (size_t)h * G) * kHeadDim + i]);
@@ -807,8 +908,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (int blk = 0; blk < nblk; ++blk)
           for (int kb = 0; kb < nkb; ++kb)
             tma_load_2d(As + kb * 8192 + blk * 1024, &tmG, kb * 64, b * D.wcap + g0 + blk * 8, &barAB);
-        mbar_expect_tx(&barV, nt * kHeadDim * 2);
-        bulk_g2s(Vs, Ly.V_win + ((size_t)bh * D.wcap + req_weff(D, b) + g0) * kHeadDim, nt * kHeadDim * 2, &barV);
+        mbar_expect_tx(&barVc[0], nt * kHeadDim * 2);
+        bulk_g2s(Vs, Ly.V_win + ((size_t)bh * D.wcap + req_weff(D, b) + g0) * kHeadDim, nt * kHeadDim * 2, &barVc[0]);
       }
       if (tid < kUnitTok) tok[tid] = tid < nt ? req_s(D, b) + g0 + tid : 0;
     }
@@ -841,15 +942,16 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           atomicAdd(Ly.vc_stats + (size_t)bh * 4 + 1, 1ull);
         }
       }
-      mbar_expect_tx(&barV, kChunk * kHeadDim * 2);
-      bulk_g2s(Vs + tid * kChunk * kHeadDim, vsrc, kChunk * kHeadDim * 2, &barV);
+      mbar_expect_tx(&barVc[tid], kChunk * kHeadDim * 2);
+      bulk_g2s(Vs + tid * kChunk * kHeadDim, vsrc, kChunk * kHeadDim * 2, &barVc[tid]);
     } else if (kind == 0 && tid < kUnitTok && tid >= nch * kChunk) {
       tok[tid] = 0;                                      // padded rows (masked below)
     }
     ntok = kind == 0 ? nch * kChunk : min(kUnitTok, n_gen - ui * kUnitTok);
     if (early_next) pdl_trigger();                       // next layer's score may become resident
     trace(2, 2);
-    if (D.serial) mbar_wait(&barV, 0);                   // SKV_SERIALIZE: values first, then the rebuild
+    if (D.serial)                                        // SKV_SERIALIZE: values first, then the rebuild
+      for (int c = 0; c < (kind == 0 ? nch : 1); ++c) mbar_wait(&barVc[c], 0);
     // ---- K~ = A_rows . B_h on the 5th-generation tensor cores (Alg 2 "MatMul(Gather(A, I), B)"):
     //      one thread issues r/16 tcgen05.mma (M = 128 rows of which 64 are the unit's tokens, N = 128, K = 16
     //      each) into an fp32 TMEM accumulator; completion is committed to barMMA
@@ -976,16 +1078,17 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (ntok <= 0) {                 // window unit past the live window (grid sized for max_step)
       for (int hq = tid >> 7; hq < G; hq += 2) {
         const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-        o_part[row * kHeadDim + (tid & 127)] = 0.f;
-        if ((tid & 127) == 0) ml_part[row] = make_float2(-INFINITY, 0.f);
+        const unsigned tg = tagv[hq];
+        st_tagged(o_part + row * kHeadDim + (tid & 127), 0.f, tg);
+        if ((tid & 127) == 0) { st_tagged(ml_part + 2 * row, -INFINITY, tg); st_tagged(ml_part + 2 * row + 1, 0.f, tg); }
       }
       return;
     }
     if (tid == 0) {
       mbar_expect_tx(&barAB, ntok * kHeadDim * 2);
       bulk_g2s(Ks, Ksrc, ntok * kHeadDim * 2, &barAB);
-      mbar_expect_tx(&barV, ntok * kHeadDim * 2);
-      bulk_g2s(Vs, Vsrc, ntok * kHeadDim * 2, &barV);
+      mbar_expect_tx(&barVc[0], ntok * kHeadDim * 2);
+      bulk_g2s(Vs, Vsrc, ntok * kHeadDim * 2, &barVc[0]);
     }
     mbar_wait(&barAB, 0);
 #pragma unroll
@@ -1040,21 +1143,26 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (lane == 0) ml[hq] = make_float2(m, l);
   }
   trace(2, 4);
-  mbar_wait(&barV, 0);                                   // values (from PCIe for selected units)
-  trace(2, 5);
-  if (vc_id >= 0 && Ly.vc_dir) {                         // this step's selection becomes the cache (R26)
+  __syncthreads();                                       // probabilities P and ml[] complete
+  // a5 -> a6: the values of a selected-chunk unit land chunk by chunk (barVc[c]); the PV consumes them
+  // as they arrive, so only the last chunk's 8 tokens remain once the host link delivers it.  The
+  // result does not depend on the arrival order: per-chunk partial sums, combined in chunk order.
+  const int nvb = kind == 0 ? nch : 1;                   // value barriers of this unit
+  auto vc_write_back = [&]() {                           // this step's selection becomes the cache (R26)
     const int slot = ui * 8 + tid;                       // deterministic position in the selection
     fence_proxy_async();
     bulk_s2g(Ly.vc_values + (((size_t)bh * 2 + (vc_gen & 1)) * D.k + slot) * (kChunk * kHeadDim),
              Vs + tid * kChunk * kHeadDim, kChunk * kHeadDim * 2);
     Ly.vc_dir[(size_t)bh * D.n_c + vc_id] = ((vc_gen + 1) << 32) | (unsigned)slot;
-  }
-  __syncthreads();
+  };
   if constexpr (G >= 8) {
     // ---- PV on the tensor cores: O[16][128] = P[16][64] . V[64][128], mma.sync m16n8k8 TF32 (values bf16:
-    //      exact; probabilities rounded to TF32); warp w owns dims 16w..16w+15
+    //      exact; probabilities rounded to TF32); warp w owns dims 16w..16w+15; k step c = chunk c, taken
+    //      in chunk order as each chunk lands
     float c[2][4];
-    pv_tile_mma<G>(P, Vs, ntok, warp, lane, c);
+    pv_tile_mma<G>(P, Vs, ntok, warp, lane, c, barVc, kind == 0);
+    trace(2, 5);
+    if (vc_id >= 0 && Ly.vc_dir) vc_write_back();
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -1064,23 +1172,54 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const int hq = g + 8 * hh;
         if (hq < G) {
           const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-          *reinterpret_cast<float2*>(o_part + row * kHeadDim + dim) = make_float2(c[nt][2 * hh], c[nt][2 * hh + 1]);
-          if (warp == 0 && t == 0) ml_part[row] = ml[hq];
+          st_tagged(o_part + row * kHeadDim + dim, c[nt][2 * hh], tagv[hq]);
+          st_tagged(o_part + row * kHeadDim + dim + 1, c[nt][2 * hh + 1], tagv[hq]);
+          if (warp == 0 && t == 0 && nt == 1) {
+            st_tagged(ml_part + 2 * row, ml[hq].x, tagv[hq]); st_tagged(ml_part + 2 * row + 1, ml[hq].y, tagv[hq]);
+          }
         }
       }
     }
   } else {
-    // ---- PV: thread = (dim pair, head group of 4): bf16x2 value loads, float4 probability loads
-    {
-      const int dp = tid & 63, grp = tid >> 6;
-      const int ntok4 = (ntok + 3) & ~3;                   // P is 0 past ntok; stale V rows are skipped
-      for (int hq = grp; hq < G; hq += 4) {
-        const float* ph = P + hq * kPStride;
+    // ---- PV: thread = (dim pair dp, q row hq < G <= 4): bf16x2 value loads, float4 probability loads
+    const int dp = tid & 63, hq = tid >> 6;
+    if (hq < G) {
+      const float* ph = P + hq * kPStride;
+      float2 acc = make_float2(0.f, 0.f);
+      if (kind == 0) {
+        float2 pc[8];                                    // per-chunk partial sums
+        unsigned pending = (1u << nvb) - 1u;
+        while (pending) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (((pending >> c) & 1u) && mbar_test(&barVc[c], 0)) {
+              pending &= ~(1u << c);
+              const float4 p0 = *reinterpret_cast<const float4*>(ph + 8 * c);
+              const float4 p1 = *reinterpret_cast<const float4*>(ph + 8 * c + 4);
+              const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+              float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t v2 = *reinterpret_cast<const uint32_t*>(Vs + (8 * c + e) * kHeadDim + 2 * dp);
+                a.x = fmaf(pp[e], bf_lo(v2), a.x);
+                a.y = fmaf(pp[e], bf_hi(v2), a.y);
+              }
+              pc[c] = a;
+              if (tid == c && vc_id >= 0 && Ly.vc_dir) vc_write_back();
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < nvb) { acc.x += pc[c].x; acc.y += pc[c].y; }
+      } else {
+        mbar_wait(&barVc[0], 0);
+        const int ntok4 = (ntok + 3) & ~3;               // P is 0 past ntok; stale V rows are skipped
         float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
         for (int t = 0; t < ntok4; t += 4) {
           const float4 p4 = *reinterpret_cast<const float4*>(ph + t);
           const float pp[4] = {p4.x, p4.y, p4.z, p4.w};
-  #pragma unroll
+#pragma unroll
           for (int e = 0; e < 4; ++e) {
             const uint32_t v2 = t + e < ntok ? *reinterpret_cast<const uint32_t*>(Vs + (t + e) * kHeadDim + 2 * dp) : 0u;
             float2& a = (e & 1) ? a1 : a0;
@@ -1088,11 +1227,14 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             a.y = fmaf(pp[e], bf_hi(v2), a.y);
           }
         }
-        const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
-        *reinterpret_cast<float2*>(o_part + row * kHeadDim + 2 * dp) = make_float2(a0.x + a1.x, a0.y + a1.y);
-        if (dp == 0) ml_part[row] = ml[hq];
+        acc = make_float2(a0.x + a1.x, a0.y + a1.y);
       }
+      const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
+      st_tagged(o_part + row * kHeadDim + 2 * dp, acc.x, tagv[hq]);
+      st_tagged(o_part + row * kHeadDim + 2 * dp + 1, acc.y, tagv[hq]);
+      if (dp == 0) { st_tagged(ml_part + 2 * row, ml[hq].x, tagv[hq]); st_tagged(ml_part + 2 * row + 1, ml[hq].y, tagv[hq]); }
     }
+    trace(2, 5);
   }
   if (vc_id >= 0 && Ly.vc_dir) bulk_wait_read();         // the cache write-back has read its smem
   if (rebuild) {                                         // every TMEM read finished (tcgen05.ld waited)
@@ -1141,17 +1283,17 @@ size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base) {
   char* p_z = carve(BHk * D.n_c * 4);                // select fallback / large-n_c slices
   char* p_sel = carve(BHk * D.k * 4);                // definite selections (and the radix fallback)
   char* p_rest = carve(BHk * D.k * 4);               // threshold-bucket selections
-  char* p_op = carve(BHq * n_split * kHeadDim * 4);
-  char* p_ml = carve(BHq * n_split * 8);
+  char* p_op = carve(BHq * n_split * kHeadDim * 8);  // {value, tag} pairs
+  char* p_ml = carve(BHq * n_split * 16);
   if (ws) {
     ws->logits = reinterpret_cast<float*>(p_log);
     ws->part = reinterpret_cast<float2*>(p_part);
     ws->z = reinterpret_cast<float*>(p_z);
     ws->sel = reinterpret_cast<int32_t*>(p_sel);
-    ws->o_part = reinterpret_cast<float*>(p_op);
-    ws->ml_part = reinterpret_cast<float2*>(p_ml);
-    ws->counters = reinterpret_cast<int*>(base);
-    ws->flags = reinterpret_cast<int*>(base) + (size_t)D.b * D.hk;
+    ws->o_part = reinterpret_cast<uint2*>(p_op);
+    ws->ml_part = reinterpret_cast<uint2*>(p_ml);
+    ws->flags = reinterpret_cast<int*>(base);
+    ws->epochs = reinterpret_cast<int*>(base) + (size_t)D.b * D.hk * 4;
     ws->selrest = reinterpret_cast<int32_t*>(p_rest);
     ws->n_sblk = tph;
     ws->n_split = n_split;
@@ -1171,23 +1313,15 @@ static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// Relay grid after k_sparse_attn (no body, no griddepcontrol.wait).  Measured
-// (tools/probe_pdl.cu): when a grid reads host-mapped memory, a PDL dependent that waits on it
-// directly is released ~4.5 us after its last CTA exits, against ~0.8 us otherwise.  With this
-// grid in between, the next kernel's griddepcontrol.wait still orders it after k_sparse_attn
-// (stream order) but is released ~0.8 us after it, i.e. 3.7 us earlier per layer.
-__global__ void k_relay() { pdl_trigger(); }
-
 // tuning switches (process environment, read once); the test hooks SKV_NO_TC and
 // SKV_SELECT_FALLBACK are read per call because tests toggle them inside one process
 struct Tuning {
-  int early_next, relay, merge_late;
+  int early_next, merge_late;
 };
 static const Tuning& tuning() {
   static const Tuning t = [] {
     auto is = [](const char* name, char c) { const char* v = getenv(name); return v && v[0] == c; };
-    return Tuning{is("SKV_SPARSE_TRIGGER", '0') ? 0 : 1, is("SKV_NO_RELAY", '1') ? 0 : 1,
-                  is("SKV_MERGE_TRIGGER", 'l') ? 1 : 0};
+    return Tuning{is("SKV_SPARSE_TRIGGER", '0') ? 0 : 1, is("SKV_MERGE_TRIGGER", 'l') ? 1 : 0};
   }();
   return t;
 }
@@ -1298,20 +1432,16 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     return cudaErrorInvalidValue;
   nvtxRangePushA("skv::sparse_attn");
   e = launch_pdl(!D.serial, k_sparse_attn<G>, dim3(units), dim3(256), (size_t)lay.bytes, st, tmA, tmB, tmG, D, R, Ly, q,
-                      ws.sel, ws.flags, step, ws.o_part, ws.ml_part,
+                      ws.sel, ws.flags, step, ws.o_part, ws.ml_part, (const int*)ws.epochs,
                       n_sel_u, n_out_u, n_win_u, n_gen_u, n_split, scale, dbg_keys, early_next);
   nvtxRangePop();
   if (e) return e;
   if (prof) profile_mark(prof, kSparseAttn, true, st);
-  if (tuning().relay) {                                  // SKV_NO_RELAY=1 omits the relay grid
-    if ((e = launch_pdl(!D.serial, k_relay, dim3(1), dim3(32), 0, st))) return e;
-    *launches += 1;
-  }
   const int merge_late = tuning().merge_late;            // SKV_MERGE_TRIGGER=late: after the loads
   if (prof) profile_mark(prof, kCombine, false, st);
   nvtxRangePushA("skv::merge");
   e = launch_pdl(!D.serial, k_merge<G>, dim3(D.b * D.hq), dim3(kHeadDim), (size_t)n_split * (sizeof(float2) + sizeof(float)), st, D,
-                      (const float*)ws.o_part, (const float2*)ws.ml_part, n_split, ws.sel, ws.flags, out,
+                      (const uint2*)ws.o_part, (const uint2*)ws.ml_part, ws.epochs, n_split, ws.sel, ws.flags, out,
                       merge_late, Ly.vc_stats);
   nvtxRangePop();
   if (e) return e;

@@ -57,16 +57,17 @@ struct BuildWs {
   float* negm;       // [b][hk][n_c]  (-m, keys for the outlier top-o)
 };
 struct DecodeWs {
-  int* counters;     // [b][hk] zero-initialised by the caller once; every call leaves them zero
-  int* flags;        // [b][hk][4] {score_done, slots_reserved, -, -}; zeroed again by each call's merger
+  int* flags;        // [b][hk][4] {score_done, -, -, -}; zeroed again by each call's merger
+  int* epochs;       // [b][hq] calls merged so far per query row (zero-initialised once): the sparse units
+                     // tag this call's partials with epoch + 1, the merge waits for that tag, then bumps
   int32_t* selrest;  // [b][hk][k] radix-fallback scratch (top-k, ascending)
   float* logits;     // [b][hk][n_c][G]: landmark-major, the G rows of a landmark contiguous (one vector
                      // store in the score epilogue, one vector load per landmark in k_select)
   float2* part;      // [b][hq][tiles_per_head] per-tile softmax partials (max, sumexp) of each query row
   float* z;          // [b][hk][n_c]     (only when n_c does not fit the select kernel's smem)
   int32_t* sel;      // [b][hk][k] published selection, unordered, chunk id + 1 (0 = not yet); re-zeroed
-  float* o_part;     // [b][hq][n_split][d]
-  float2* ml_part;   // [b][hq][n_split]
+  uint2* o_part;     // [b][hq][n_split][d]  {fp32 bits, tag}: 8-byte value + flag pairs
+  uint2* ml_part;    // [b][hq][n_split][2]  {m bits, tag}, {l bits, tag}
   int n_sblk, n_split;
 };
 
@@ -76,10 +77,13 @@ constexpr int kUnitTok = 64;                      // tokens per attention unit (
 constexpr size_t kSelectSmemMax = 160 * 1024;     // per-CTA z slice + its logits kept in smem
 constexpr int kSelCL = 8;                         // select: CTAs per (request, KV head) cluster
 constexpr int kSelThreads = 512;
-constexpr int kSelCandLocal = 1024;               // threshold-bucket candidates per CTA
+constexpr int kSelCandLocal = 1024;               // threshold-bucket candidates of a cluster (all ranks)
+constexpr int kSelCandPush = 128;                 // threshold-bucket candidates per CTA (more: radix fallback)
 
-// header: per-(b,h) merge counter + 4 selection flags {def_ready, n_def, rest_ready, n_rest}
-inline size_t ws_header_bytes(const Dims& D) { return ((size_t)D.b * D.hk * 5 * 4 + 255) & ~(size_t)255; }
+// header (zero-filled once by the caller): 4 flags per (b, h_kv), then one partial epoch per query row
+inline size_t ws_header_bytes(const Dims& D) {
+  return (((size_t)D.b * D.hk * 4 + (size_t)D.b * D.hq) * 4 + 255) & ~(size_t)255;
+}
 size_t build_ws_bytes(const Dims& D, BuildWs* ws, char* base);
 size_t decode_ws_bytes(const Dims& D, DecodeWs* ws, char* base);
 

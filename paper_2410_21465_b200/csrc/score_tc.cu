@@ -126,6 +126,9 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
     if (tr >= 0 && tr < ntile * kSTile) atomicOr(&obits[tr >> 5], 1u << (tr & 31));
   }
   pdl_wait();                                          // everything below may read the caller's inputs
+  // every CTA of this grid is resident: the selector grid may launch now (its CTAs are dispatched the
+  // moment ours exit; its own griddepcontrol.wait orders it after this grid's logits and partials)
+  pdl_trigger();
   trace_tc(trace_buf, 15);
   // B operands (q of each KV head in range, K-major SWIZZLE_128B, rows n >= G zero) and the a7
   // window append (R18): call inputs, after the wait
@@ -263,7 +266,6 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
   }
   __syncthreads();
   trace_tc(trace_buf, 1);
-  pdl_trigger();
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" :: "r"(tmem));

@@ -21,6 +21,7 @@ ap.add_argument("--slots", type=int, default=1, help="trace this many consecutiv
 ap.add_argument("--vc-rho", type=float, default=None, help="value cache on, queries drifting with this rho")
 ap.add_argument("--q-len", type=int, default=1, help="s_q query tokens per call")
 args = ap.parse_args()
+args.layers = max(args.layers, args.slots)
 os.environ["SKV_TRACE_SLOTS"] = str(args.slots)
 cfg = synth.CONFIGS[args.config]
 shape = Shape.from_config(cfg, steps=64, q_len=args.q_len)
@@ -79,7 +80,7 @@ if args.slots > 1:
 t = T[args.slots - 1]
 t0 = t[0][t[0][:, 0] > 0][:, 0].min()
 names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done", "epi_t0", "epi_t1", "epi_t2", "epi_t3", "mma0_issued", "epi_loop_done", "flushed", "pdl_released"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "B_found", "pass1_done", "emitted", "nseg", "loaded_max", "exp_sum"],
-         3: ["merge_start", "merge_done"],
+         3: ["merge_start", "merge_done", "ml_ready"],
          2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end", "pv_done", "synced", "exit"]}
 for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
     m = t[kid]
