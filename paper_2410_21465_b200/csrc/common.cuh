@@ -123,6 +123,7 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // G consecutive floats (16-byte aligned when G % 4 == 0) stored / loaded as vectors
 template <int G>

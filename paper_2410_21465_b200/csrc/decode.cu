@@ -688,24 +688,19 @@ k_merge(Dims D, const uint2* __restrict__ o_part, const uint2* __restrict__ ml_p
   }
   __syncthreads();                                        // every unit's (m, l) has landed
   trace(3, 2);
-  constexpr int kBatch = 64;                              // partial loads in flight per thread
-  float v[kBatch];
-  auto load_o = [&](int s0) {                             // (a value may trail its unit's (m, l): re-poll)
-    uint2 t[kBatch];
+  // this thread's values of the first kBatch units: loads issued now, consumed after the weights
+  constexpr int kBatch = 64;
+  uint2 t[kBatch];
+  auto issue_o = [&](int s0) {
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) t[u] = s0 + u < n_split ? ld_tagged(orow + (size_t)(s0 + u) * kHeadDim) : make_uint2(0u, tag);
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      while (t[u].y != tag) { __nanosleep(32); t[u] = ld_tagged(orow + (size_t)(s0 + u) * kHeadDim); }
-      v[u] = __uint_as_float(t[u].x);
-    }
   };
-  load_o(0);
+  issue_o(0);
+  trace(3, 3);
   // weights, computed once per CTA: M = max_s m_s; w_s = exp(m_s - M); L = sum_s l_s w_s
   __shared__ float red[kHeadDim / 32];
   float* w = reinterpret_cast<float*>(mls + n_split);     // [n_split]
   const int lane = d & 31, warp = d >> 5;
-  __syncthreads();
   float mx = -INFINITY;
   for (int s2 = d; s2 < n_split; s2 += kHeadDim) mx = fmaxf(mx, mls[s2].x);
   mx = warp_max(mx);
@@ -728,12 +723,22 @@ k_merge(Dims D, const uint2* __restrict__ o_part, const uint2* __restrict__ ml_p
   float L = 0.f;
 #pragma unroll
   for (int i = 0; i < kHeadDim / 32; ++i) L += red[i];    // fixed order: deterministic
+  trace(3, 4);
   float acc = 0.f;
   for (int s0 = 0; s0 < n_split; s0 += kBatch) {
-    if (s0 > 0) load_o(s0);
+    if (s0 > 0) issue_o(s0);
+    for (;;) {                                            // (a value may trail its unit's (m, l): the
+      unsigned long long stale = 0ull;                    //  stale ones are re-read together)
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) stale |= (unsigned long long)(t[u].y != tag) << u;
+      if (!stale) break;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u)
+        if ((stale >> u) & 1ull) t[u] = ld_tagged(orow + (size_t)(s0 + u) * kHeadDim);
+    }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
-      if (s0 + u < n_split) acc = fmaf(w[s0 + u], v[u], acc);
+      if (s0 + u < n_split) acc = fmaf(w[s0 + u], __uint_as_float(t[u].x), acc);
   }
   if (late_trigger) pdl_trigger();                        // the next grid's prefetch after our loads
   out[(size_t)row * kHeadDim + d] = f2bf(acc / L);
@@ -1174,9 +1179,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
           st_tagged(o_part + row * kHeadDim + dim, c[nt][2 * hh], tagv[hq]);
           st_tagged(o_part + row * kHeadDim + dim + 1, c[nt][2 * hh + 1], tagv[hq]);
-          if (warp == 0 && t == 0 && nt == 1) {
-            st_tagged(ml_part + 2 * row, ml[hq].x, tagv[hq]); st_tagged(ml_part + 2 * row + 1, ml[hq].y, tagv[hq]);
-          }
         }
       }
     }
@@ -1232,11 +1234,18 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const size_t row = ((size_t)b * D.hq + (size_t)h * G + hq) * n_split + split;
       st_tagged(o_part + row * kHeadDim + 2 * dp, acc.x, tagv[hq]);
       st_tagged(o_part + row * kHeadDim + 2 * dp + 1, acc.y, tagv[hq]);
-      if (dp == 0) { st_tagged(ml_part + 2 * row, ml[hq].x, tagv[hq]); st_tagged(ml_part + 2 * row + 1, ml[hq].y, tagv[hq]); }
     }
     trace(2, 5);
   }
-  if (vc_id >= 0 && Ly.vc_dir) bulk_wait_read();         // the cache write-back has read its smem
+  // (m, l) last, once every thread has stored its values (and the value-cache write-back has completed:
+  // the merge then closes the generation): the merge polls (m, l) first
+  if (vc_id >= 0 && Ly.vc_dir) bulk_wait_all();
+  __syncthreads();
+  if (tid < G) {
+    const size_t row = ((size_t)b * D.hq + (size_t)h * G + tid) * n_split + split;
+    st_tagged(ml_part + 2 * row, ml[tid].x, tagv[tid]);
+    st_tagged(ml_part + 2 * row + 1, ml[tid].y, tagv[tid]);
+  }
   if (rebuild) {                                         // every TMEM read finished (tcgen05.ld waited)
     tc_fence_before();
     __syncthreads();
@@ -1447,6 +1456,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (e) return e;
   if (prof) profile_mark(prof, kCombine, true, st);
   *launches += 4;
+
   return cudaGetLastError();
 }
 

@@ -80,7 +80,7 @@ if args.slots > 1:
 t = T[args.slots - 1]
 t0 = t[0][t[0][:, 0] > 0][:, 0].min()
 names = {0: ["start", "end", "tile0_in", "tile1_in", "tile2_in", "tile3_in", "setup_smem", "setup_done", "epi_t0", "epi_t1", "epi_t2", "epi_t3", "mma0_issued", "epi_loop_done", "flushed", "pdl_released"], 1: ["start", "pdl_done", "lse", "z_hist", "sync1", "cand_scan", "sync2", "end", "gathered", "ranked", "B_found", "pass1_done", "emitted", "nseg", "loaded_max", "exp_sum"],
-         3: ["merge_start", "merge_done", "ml_ready"],
+         3: ["merge_start", "merge_done", "ml_ready", "o_issued", "weights"],
          2: ["start", "pdl_done", "issued", "AB_in", "logits", "V_in", "partial_done", "merge_end", "pv_done", "synced", "exit"]}
 for kid, kn in [(0, "score"), (1, "select"), (2, "sparse_attn"), (3, "merge")]:
     m = t[kid]
