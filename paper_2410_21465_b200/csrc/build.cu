@@ -30,10 +30,11 @@ static __device__ __forceinline__ int* tile_tok_ptr(uint8_t* smem, int r) {
 // block kb at kb * 16 KB) | B_h MN-major SWIZZLE_128B (two boxes of r rows x 64 columns); the fp32 key
 // tile aliases both once the MMAs have completed.
 constexpr int kKsStride = kHeadDim + 4;               // floats: 528-byte rows, conflict-free 16 B stores
+constexpr int kChunksPerTile = kTileTok / kChunk;    // 16
 __host__ __device__ constexpr size_t build_tc_smem_bytes(int r) {
   const size_t ab = (size_t)((r + 63) / 64) * 16384 + (size_t)2 * r * 128;
   const size_t ks = (size_t)kTileTok * kKsStride * 4;
-  return (ab > ks ? ab : ks) + kTileTok * sizeof(int) + 1024;
+  return (ab > ks ? ab : ks) + kTileTok * sizeof(int) + (size_t)kChunksPerTile * (kKsStride + 1) * 4 + 1024;
 }
 constexpr uint32_t kIdescBuild = umma_idesc_bf16(128, 128, false, true);
 
@@ -125,39 +126,64 @@ k_build_chunks(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     build_key_tile_tc(&tmA, &tmB, b * D.s + j0 * kChunk, (int)bh * D.r, D.r, R, tok, smem, Ks, &bar_ab, &bar_mma,
                       &tmem_slot);
   }
-  // warp w: chunks 2w, 2w+1 of the tile; lane: dims 4*lane..+4
+  // chunk statistics from the fp32 key tile.  (A) thread (chunk c, dims 8q..8q+8):
+  // C_j = (1/c) sum of the chunk's keys -> landmark row (bf16) and |C_j|^2 (16-lane reduction);
+  // (B) thread (token t, half of the dims): <C_j, k_t> and |k_t|^2 (pair reduction), cos (zero norm
+  // -> -1), m_j = min over the chunk's 8 tokens (16-lane reduction).  No per-row warp sums.
+  float* Cs = reinterpret_cast<float*>(tok + kTileTok);          // [16][kKsStride] chunk means
+  float* Cn = Cs + kChunksPerTile * kKsStride;                   // [16] |C_j|
+  {
+    const int c = tid >> 4, q = tid & 15, j = j0 + c;
+    float acc[8];
 #pragma unroll
-  for (int cc = 0; cc < 2; ++cc) {
-    const int jl = warp * 2 + cc, j = j0 + jl;
-    if (j >= D.n_c) break;
-    if (j >= ncb) {                                     // padding past a shorter request's grid: never
-      const size_t row = bh * D.n_c + j;                // an outlier (-m = -inf), landmark row zero
-      if (lane == 0) { mincos[row] = INFINITY; negm[row] = -INFINITY; }
-      *reinterpret_cast<uint2*>(Ly.L + row * kHeadDim + lane * 4) = make_uint2(0u, 0u);
-      continue;
-    }
-    float4 kv[kChunk];
-    float4 C = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll
     for (int u = 0; u < kChunk; ++u) {
-      kv[u] = *reinterpret_cast<const float4*>(Ks + (jl * kChunk + u) * kKsStride + lane * 4);
-      C.x += kv[u].x; C.y += kv[u].y; C.z += kv[u].z; C.w += kv[u].w;
+      const float4* kr = reinterpret_cast<const float4*>(Ks + (c * kChunk + u) * kKsStride + q * 8);
+      const float4 x = kr[0], y = kr[1];
+      acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
+      acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
     }
-    C.x *= 0.125f; C.y *= 0.125f; C.z *= 0.125f; C.w *= 0.125f;       // (1/c) sum, c = 8
-    const float cn = sqrtf(warp_sum(C.x * C.x + C.y * C.y + C.z * C.z + C.w * C.w));
-    float m = INFINITY;
+    float c2 = 0.f;
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u) {
-      float dot = warp_sum(C.x * kv[u].x + C.y * kv[u].y + C.z * kv[u].z + C.w * kv[u].w);
-      float kn = sqrtf(warp_sum(kv[u].x * kv[u].x + kv[u].y * kv[u].y + kv[u].z * kv[u].z + kv[u].w * kv[u].w));
-      float den = cn * kn;
-      float cosv = den > 0.f ? dot / den : -1.f;                        // zero norm -> -1
-      m = fminf(m, cosv);
+    for (int e = 0; e < 8; ++e) { acc[e] *= 0.125f; c2 = fmaf(acc[e], acc[e], c2); }   // (1/c) sum, c = 8
+    float4* cr = reinterpret_cast<float4*>(Cs + c * kKsStride + q * 8);
+    cr[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    cr[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+    if (q == 0) Cn[c] = sqrtf(c2);
+    if (j < D.n_c) {
+      const size_t row = bh * D.n_c + j;
+      uint4 pk = make_uint4(0u, 0u, 0u, 0u);               // padding past a shorter request's grid: zero row
+      if (j < ncb) pk = make_uint4(pack_bf2(acc[0], acc[1]), pack_bf2(acc[2], acc[3]), pack_bf2(acc[4], acc[5]),
+                                   pack_bf2(acc[6], acc[7]));
+      *reinterpret_cast<uint4*>(Ly.L + row * kHeadDim + q * 8) = pk;
     }
-    const size_t row = bh * D.n_c + j;
-    if (lane == 0) { mincos[row] = m; negm[row] = -m; }
-    uint2 pk = make_uint2(pack_bf2(C.x, C.y), pack_bf2(C.z, C.w));
-    *reinterpret_cast<uint2*>(Ly.L + row * kHeadDim + lane * 4) = pk;
+  }
+  __syncthreads();
+  {
+    const int t = tid >> 1, hf = tid & 1, c = t >> 3, j = j0 + c;
+    const float4* kr = reinterpret_cast<const float4*>(Ks + t * kKsStride + hf * 64);
+    const float4* cr = reinterpret_cast<const float4*>(Cs + c * kKsStride + hf * 64);
+    float dot = 0.f, k2 = 0.f;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float4 x = kr[e], y = cr[e];
+      dot = fmaf(x.x, y.x, dot); dot = fmaf(x.y, y.y, dot); dot = fmaf(x.z, y.z, dot); dot = fmaf(x.w, y.w, dot);
+      k2 = fmaf(x.x, x.x, k2); k2 = fmaf(x.y, x.y, k2); k2 = fmaf(x.z, x.z, k2); k2 = fmaf(x.w, x.w, k2);
+    }
+    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+    k2 += __shfl_xor_sync(0xffffffffu, k2, 1);
+    const float den = Cn[c] * sqrtf(k2);
+    float m = den > 0.f ? dot / den : -1.f;                  // zero norm -> -1
+#pragma unroll
+    for (int o = 2; o < 16; o <<= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 15) == 0 && j < D.n_c) {
+      const size_t row = bh * D.n_c + j;
+      if (j < ncb) { mincos[row] = m; negm[row] = -m; }
+      else { mincos[row] = INFINITY; negm[row] = -INFINITY; } // padding: never an outlier
+    }
   }
 }
 

@@ -326,9 +326,10 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   pdl_wait();
   trace(1, 1);
   int* fl = flags + bh * 4;
-  // score (incl. a7 window append) complete; the release store is left to the last warp, which has no
-  // lse work (warps < G are on the critical path)
-  if (crank == 0 && tid == NT - 32) st_release_gpu(&fl[0], 1);
+  // score (incl. a7 window append) complete.  A relaxed store: the score grid's writes reached L2 when it
+  // completed (our griddepcontrol.wait), and the readers (outlier / window units) bulk-copy from L2; a
+  // release here is a membar on the critical path of the barrier below
+  if (crank == 0 && tid == NT - 32) st_relaxed_gpu(&fl[0], 1);
   // ---- lse_hq from the score kernel's per-tile partials (warps < G) and the first z-pass logits: both
   //      load batches are issued before either is used (their L2 latencies overlap).  Each lane merges
   //      its tiles lane, lane+32, ... in batches of 8 (batch max, then one sum of 8 independent exps),
