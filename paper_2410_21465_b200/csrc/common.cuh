@@ -246,19 +246,25 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
 __device__ __forceinline__ void st_relaxed_gpu(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+// Bounded polling: a flag that never arrives (a bug, or a grid that cannot become resident) aborts the
+// kernel with an error after ~2 s instead of hanging the device.  Call with the spin's start time.
+__device__ __forceinline__ void spin_guard(uint64_t t0) {
+  if (globaltimer() - t0 > 2000000000ull) __trap();
+}
 // spin (with backoff) until flag[0] != 0, then return flag[1] (read with acquire semantics by one
 // thread and broadcast through shared memory, so no thread can see a stale L1 copy)
 __device__ __forceinline__ int cta_wait_flag(const int* flag) {
   __shared__ int bcast;
   __syncthreads();
   if (threadIdx.x == 0) {
-    while (ld_acquire_gpu(flag) == 0) __nanosleep(64);
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_gpu(flag) == 0) { __nanosleep(64); spin_guard(t0); }
     bcast = ld_acquire_gpu(flag + 1);
   }
   __syncthreads();
   return bcast;
-}
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
 }
 }  // namespace skv

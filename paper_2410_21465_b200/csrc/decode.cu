@@ -680,10 +680,12 @@ k_merge(Dims D, const uint2* __restrict__ o_part, const uint2* __restrict__ ml_p
   const uint2* orow = o_part + (size_t)row * n_split * kHeadDim + d;
   for (int i = d; i < n_split; i += kHeadDim) {           // (m, l) of every unit, polled with back-off
     uint2 m2, l2;
+    const uint64_t t0 = globaltimer();
     for (;;) {
       m2 = ld_tagged(mr + 2 * i); l2 = ld_tagged(mr + 2 * i + 1);
       if (m2.y == tag && l2.y == tag) break;
       __nanosleep(128);
+      spin_guard(t0);
     }
     mls[i] = make_float2(__uint_as_float(m2.x), __uint_as_float(l2.x));
   }
@@ -924,7 +926,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (kind == 0 && tid < nch) {                        // (generated units set their positions above)
       const int* sp = slots + ui * 8 + tid;
       int v;
-      while ((v = ld_relaxed_gpu(sp)) == 0) __nanosleep(32);
+      const uint64_t t0 = globaltimer();
+      while ((v = ld_relaxed_gpu(sp)) == 0) { __nanosleep(32); spin_guard(t0); }
       const int id = v - 1;
       vc_id = id;
 #pragma unroll
