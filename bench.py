@@ -59,6 +59,9 @@ def parse():
                     help="value-cache leg (P:156, DESIGN R26/R27): comma list of query-drift correlations rho; "
                          "each runs the same step with a GPU value cache per layer and drifting queries and "
                          "reports the measured hit rate alpha ('' = skip)")
+    ap.add_argument("--vc-capacity", default="1,4",
+                    help="value-cache legs: comma list of capacities in units of the budget k (C = m * k chunks per "
+                         "request and KV head; least-recently-selected replacement, DESIGN R26)")
     ap.add_argument("--q-len-leg", type=int, default=4,
                     help="multi-query leg (NEXT-3, Alg 2's s_q): the same 32-layer step with s_q query tokens per "
                          "call (speculative verification); 0 = skip")
@@ -328,7 +331,7 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------------------------------------
-def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_bytes, host_peak, n_total, dev):
+def value_cache_leg(args, cfg, rho, capacity, states, rope, ws, out, stream, seed, host_bytes, host_peak, n_total, dev):
     """NEXT-1: the same 32-layer step with a GPU value-chunk cache per layer (skv_layer.vc_*,
     capacity k chunks per request and KV head, DESIGN R26) and temporally correlated queries (AR(1) drift
     over decode steps, synth.gen_q_drift, R27).  Hit rate alpha is read from the kernels' own counters.
@@ -343,10 +346,12 @@ def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_by
         layers = []
         for l in range(Lm):                    # each layer its own cache, even where layer states are shared
             st = copy.copy(states[l % n_states])
-            st.vc_values = torch.empty(b, cfg.n_kv_heads, 2, cfg.budget * cfg.chunk, cfg.head_dim,
-                                       dtype=torch.bfloat16, device=dev)
+            C = capacity * cfg.budget
+            st.vc_capacity = C
+            st.vc_values = torch.empty(b, cfg.n_kv_heads, C, cfg.chunk, cfg.head_dim, dtype=torch.bfloat16, device=dev)
             st.vc_dir = torch.zeros(b, cfg.n_kv_heads, st.shape.n_c, dtype=torch.int64, device=dev)
             st.vc_stats = torch.zeros(b, cfg.n_kv_heads, 4, dtype=torch.int64, device=dev)
+            st.vc_slots = torch.zeros(b, cfg.n_kv_heads, C + cfg.budget, dtype=torch.int64, device=dev)
             layers.append(st)
         qd = torch.stack([synth.gen_q_drift(cfg, seed + 104729, l, warm + steps, rho, device=dev)
                           for l in range(Lm)], dim=1)               # [step][layer][b][hq][d]
@@ -363,7 +368,7 @@ def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_by
             layers[l].decode_dev(rope.struct, q_g[l], k_g[l], v_g[l], step_dev, n_total, out[l], ws, stream=cap)
         step_dev.add_(1)
     for st in layers:
-        st.vc_dir.zero_(); st.vc_stats.zero_()
+        st.vc_dir.zero_(); st.vc_stats.zero_(); st.vc_slots.zero_()
     step_dev.fill_(0)
     torch.cuda.synchronize()
     for i in range(warm):
@@ -396,14 +401,16 @@ def value_cache_leg(args, cfg, rho, states, rope, ws, out, stream, seed, host_by
     dense_bytes = 2.0 * S * cfg.head_dim * 2 * cfg.n_kv_heads * b
     beq_model = 2.0 * S * hbm_gbs / (S / C + 2.0 * (K + O) * C + (1.0 - alpha) * K * C * hbm_gbs / host_peak)
     beq_meas = dense_bytes / (ms * 1e-3 / Lm) / 1e9
-    return {"q_drift_rho": rho, "alpha": alpha, "value": value, "unit": UNIT, "ms_per_step": ms,
+    return {"q_drift_rho": rho, "capacity_chunks": capacity * cfg.budget, "capacity_over_k": capacity,
+            "alpha": alpha, "value": value, "unit": UNIT, "ms_per_step": ms,
             "equivalent_bandwidth_GBps": {"measured": beq_meas, "paper_model_P204": beq_model, "hbm_peak": hbm_gbs,
                                           "host_peak": host_peak},
             "steps": steps, "warmup": warm, "host_bytes_per_layer": miss_bytes,
             "step_frac_of_host_roofline": t_roof / (ms * 1e-3),
-            "note": "P:156 cache-aware decode: chunks selected in the previous step come from HBM (capacity k, "
-                    "least-recently-selected == previous selection); alpha measured by the kernels' hit counters; "
-                    "queries drift as AR(1) over steps (synthetic: the paper's ~60% is Fig 3c on real traces)"}
+            "note": "P:156 cache-aware decode: cached chunks come from HBM (least-recently-selected replacement, "
+                    "capacity C chunks per request and KV head; C = k keeps exactly the previous selection); alpha "
+                    "measured by the kernels' hit counters; queries drift as AR(1) over steps (synthetic: the "
+                    "paper's ~60% is Fig 3c on real traces)"}
 
 
 # ------------------------------------------------------------------------------------------------
@@ -759,8 +766,9 @@ def run_ours(args, cfg):
 
     value_cache = None
     if args.vc_rho:
-        value_cache = [leg(value_cache_leg, args, cfg, float(r), states, rope, ws, out, stream, seed, host_bytes,
-                           host_peak, n_total, dev) for r in args.vc_rho.split(",") if r.strip()]
+        value_cache = [leg(value_cache_leg, args, cfg, float(r), int(c), states, rope, ws, out, stream, seed,
+                           host_bytes, host_peak, n_total, dev)
+                       for r in args.vc_rho.split(",") if r.strip() for c in args.vc_capacity.split(",") if c.strip()]
 
     multi_query = None
     if args.q_len_leg and args.q_len_leg > 1:

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define SHADOWKV_ABI_VERSION 6
+#define SHADOWKV_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define SKV_API __attribute__((visibility("default")))
@@ -121,18 +121,18 @@ typedef struct {
   const uint16_t *V_host;   /* host-mapped bf16 [b][h_kv][s][d], read zero-copy over PCIe        */
   /* Optional GPU-resident value-chunk cache ("considering the temporal locality of the KV
    * cache, a cache policy can be leveraged"; "we conduct an index scan to detect the missed
-   * chunks"; policy per SPEC S:139-146, DESIGN R26): least-recently-selected replacement,
-   * capacity = the budget k chunks per (request, KV head).  With capacity k the cache after a step
-   * holds exactly that step's selection, so it is kept as two slot buffers that alternate by step
-   * (read the previous step's, write this step's).  A selected chunk whose directory entry carries
-   * the previous generation's tag is a HIT: its values are copied from HBM instead of the host link.
-   * Every selected chunk's values are written to this step's buffer.  Values are bit copies either
-   * way, so outputs do not depend on the cache state.  All three NULL = no cache; all three or none.
-   * build_cache zero-fills vc_dir and vc_stats (a new prefill starts cold); a caller may also reset
-   * the cache by zero-filling both.  Not shared between layers. */
-  uint16_t *vc_values;      /* device bf16 [b][h_kv][2][k*c][d] (two slot buffers per KV head)     */
+   * chunks"; policy per SPEC S:139-146, DESIGN R26): least-recently-SELECTED replacement at chunk
+   * granularity, capacity C = vc_capacity chunks per (request, KV head), C >= k (0 = k).  A selected chunk
+   * whose directory entry is valid is a HIT: its values are copied from its HBM slot instead of the host
+   * link.  Each MISS takes a slot: an empty one, else the least recently selected cached chunk that this
+   * step did not select (ties -> the lower chunk id is evicted first); its values are written there once
+   * they arrive.  Values are bit copies either way, so outputs do not depend on the cache state.  All four
+   * pointers NULL = no cache; all four or none.  build_cache zero-fills vc_dir, vc_stats and vc_slots (a
+   * new prefill starts cold); a caller may also reset the cache by zero-filling those three.  Not shared
+   * between layers. */
+  uint16_t *vc_values;      /* device bf16 [b][h_kv][C][c][d]: C value slots per KV head            */
   uint64_t *vc_dir;         /* device [b][h_kv][n_c]: (tag << 32) | slot; tag = generation + 1 of
-                               the step that last wrote the chunk; zero = never cached          */
+                               the step that inserted the chunk; zero = not cached              */
   uint64_t *vc_stats;       /* device [b][h_kv][4]: {generation (decode steps run), scratch,
                                hits in the last step, hits in total}; read them after a sync    */
   /* Optional low-rank storage of generated keys (P:196 footnote "new pre-RoPE keys K' can be stored
@@ -143,6 +143,12 @@ typedef struct {
    * K_win slots >= w_eff are then neither written nor read (values still go to V_win).  Exact when
    * k' lies in the span of the B rows (e.g. B from shadowkv_factorize). */
   uint16_t *A_gen;          /* device bf16 [b][window_cap][r]                                    */
+  /* value cache (continued, ABI 7): per-slot state and the capacity */
+  uint64_t *vc_slots;       /* device [b][h_kv][C + k]: slot s < C holds ((generation of its last
+                               selection + 1) << 32) | (chunk id + 1), 0 = empty; entries C.. are
+                               the step's miss -> slot assignments (scratch)                     */
+  int32_t vc_capacity;      /* C: value slots per (request, KV head); 0 = k; k <= C <= n_c       */
+  int32_t reserved0;
 } skv_layer;
 
 /* One-time setup for `device` (idempotent, thread-safe): kernel shared-memory attributes for every
@@ -182,7 +188,7 @@ SKV_API size_t shadowkv_workspace_bytes(const skv_dims *dims);
  *   outlier_ids <- the o chunks with smallest m (ties -> lower j, R12), ascending
  *   K_out, V_out <- keys / values of those chunks; values read zero-copy from V_host
  *   K_win, V_win slots [0, w_eff) <- the context tail (R8)
- * With a value cache (vc_*), zero-fills vc_dir and vc_stats (cold cache for the new context).
+ * With a value cache (vc_*), zero-fills vc_dir, vc_stats and vc_slots (cold cache for the new context).
  * Requires V_host page-locked and mapped (checked once here; SKV_ESTATE otherwise). */
 SKV_API skv_status shadowkv_build_cache(const skv_dims *dims, const skv_rope *rope, const skv_layer *layer,
                                 const uint16_t *K_rope, void *workspace, void *stream);

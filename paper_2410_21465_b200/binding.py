@@ -37,7 +37,8 @@ class SkvRope(ctypes.Structure):
 class SkvLayer(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("A", "B", "landmarks", "outlier_ids", "K_out", "V_out", "K_win", "V_win", "V_host",
-                 "vc_values", "vc_dir", "vc_stats", "A_gen")]
+                 "vc_values", "vc_dir", "vc_stats", "A_gen", "vc_slots")] + \
+        [("vc_capacity", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 class ShadowKVError(RuntimeError):
@@ -128,10 +129,11 @@ def rope_struct(rotary_dim: int, interleaved: bool, inv_freq) -> SkvRope:
 
 
 def layer_struct(A, B, landmarks, outlier_ids, K_out, V_out, K_win, V_win, V_host,
-                 vc_values=None, vc_dir=None, vc_stats=None, A_gen=None) -> SkvLayer:
+                 vc_values=None, vc_dir=None, vc_stats=None, A_gen=None, vc_slots=None,
+                 vc_capacity: int = 0) -> SkvLayer:
     return SkvLayer(_ptr(A), _ptr(B), _ptr(landmarks), _ptr(outlier_ids), _ptr(K_out), _ptr(V_out),
                     _ptr(K_win), _ptr(V_win), _ptr(V_host), _ptr(vc_values), _ptr(vc_dir), _ptr(vc_stats),
-                    _ptr(A_gen))
+                    _ptr(A_gen), _ptr(vc_slots), int(vc_capacity), 0)
 
 
 _INIT_DEVICES: set = set()

@@ -135,14 +135,21 @@ skv_status check_layer(const skv_layer* l, const skv::Dims& D, skv::Layer* Ly) {
     if (p.need && !p.p) return fail(SKV_EINVAL, "layer.%s is NULL", p.n);
     if (p.p && !aligned16(p.p)) return fail(SKV_EINVAL, "layer.%s is not 16-byte aligned", p.n);
   }
-  const int n_vc = (l->vc_values != nullptr) + (l->vc_dir != nullptr) + (l->vc_stats != nullptr);
-  if (n_vc != 0 && n_vc != 3) return fail(SKV_EINVAL, "layer.vc_values / vc_dir / vc_stats: give all three or none");
-  if (n_vc && (!aligned16(l->vc_values) || !aligned16(l->vc_dir) || !aligned16(l->vc_stats)))
+  const int n_vc = (l->vc_values != nullptr) + (l->vc_dir != nullptr) + (l->vc_stats != nullptr) +
+                   (l->vc_slots != nullptr);
+  if (n_vc != 0 && n_vc != 4)
+    return fail(SKV_EINVAL, "layer.vc_values / vc_dir / vc_stats / vc_slots: give all four or none");
+  if (n_vc && (!aligned16(l->vc_values) || !aligned16(l->vc_dir) || !aligned16(l->vc_stats) || !aligned16(l->vc_slots)))
     return fail(SKV_EINVAL, "layer.vc_* must be 16-byte aligned");
+  const int vc_cap = l->vc_capacity == 0 ? D.k : l->vc_capacity;
+  if (n_vc && (vc_cap < D.k || vc_cap > D.n_c || vc_cap > skv::kMaxVcCapacity))
+    return fail(SKV_EINVAL, "layer.vc_capacity %d: need budget %d <= C <= min(n_c %d, %d)", (int)l->vc_capacity, D.k,
+                D.n_c, skv::kMaxVcCapacity);
   if (l->A_gen && (reinterpret_cast<uintptr_t>(l->A_gen) & 15u)) return fail(SKV_EINVAL, "layer.A_gen must be 16-byte aligned");
   *Ly = skv::Layer{l->A, l->B, l->landmarks, l->outlier_ids, l->K_out, l->V_out, l->K_win, l->V_win, l->V_host,
                    l->A_gen, l->vc_values, reinterpret_cast<unsigned long long*>(l->vc_dir),
-                   reinterpret_cast<unsigned long long*>(l->vc_stats)};
+                   reinterpret_cast<unsigned long long*>(l->vc_stats),
+                   reinterpret_cast<unsigned long long*>(l->vc_slots), n_vc ? vc_cap : 0};
   return SKV_OK;
 }
 
@@ -308,7 +315,8 @@ skv_status shadowkv_build_cache(const skv_dims* dims, const skv_rope* rope, cons
   if (Ly.vc_dir) {     // a new context starts with a cold value cache (R26)
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if ((e = cudaMemsetAsync(Ly.vc_dir, 0, (size_t)D.b * D.hk * D.n_c * 8, s)) != cudaSuccess ||
-        (e = cudaMemsetAsync(Ly.vc_stats, 0, (size_t)D.b * D.hk * 4 * 8, s)) != cudaSuccess)
+        (e = cudaMemsetAsync(Ly.vc_stats, 0, (size_t)D.b * D.hk * 4 * 8, s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(Ly.vc_slots, 0, (size_t)D.b * D.hk * (Ly.vc_cap + D.k) * 8, s)) != cudaSuccess)
       return fail(SKV_ECUDA, "value-cache reset: %s", cudaGetErrorString(e));
   }
   e = skv::launch_build(D, R, Ly, K_rope, ws, static_cast<cudaStream_t>(stream), &launches, *ctx);

@@ -266,11 +266,105 @@ __device__ __forceinline__ float group_z(const float* lg, const float* lse) {
   return zz;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Value-chunk cache (R26): least-recently-SELECTED replacement with
+// capacity C >= k slots per (request, KV head).  After a step's selection is published, one CTA per head
+//   1. reads the k selected chunks and probes the directory: a chunk inserted by an earlier step and not
+//      evicted since (1 <= tag <= generation) is a HIT in slot s (the sparse units probe the same way);
+//   2. ranks every slot by its LRS key ((last selection generation + 1) << 32 | chunk + 1; empty = 0);
+//      slots hit in this step are never victims (key = max);
+//   3. gives the misses, in selection-position order, the slots with the smallest keys in order (empty
+//      slots first, then the least recently selected chunk, ties -> the lower chunk id: the oracle's rule);
+//   4. updates the directory (evicted chunks leave it, misses enter with tag generation + 1) and the slot
+//      state (hits and misses: last selection = this generation), and publishes each miss's slot as an
+//      8-byte {slot, generation + 1} pair that the unit holding the miss polls before writing its values
+//      (no fence: the consumer checks the tag).
+// Hits are never moved (their slot is not a victim), so no slot is read and written in one step.
+struct VcArgs {
+  unsigned long long* dir;      // [b*h_kv][n_c]
+  unsigned long long* stats;    // [b*h_kv][4] {generation, ...}
+  unsigned long long* slots;    // [b*h_kv][C + k]: slot state, then the miss -> slot assignments
+  int C, Cp;                    // capacity, next power of two (bitonic sort width)
+};
+__host__ __device__ inline size_t vc_assign_smem_bytes(int k, int Cp) {
+  return (size_t)2 * k * 4 + 8 + (size_t)Cp * 12;
+}
+template <int NT>
+__device__ __noinline__ void vc_assign(const VcArgs vc, const int32_t* slots_pub, size_t bh, int n, int k,
+                                       uint8_t* smem, TopKSmem<NT>& tk) {
+  const int tid = threadIdx.x;
+  const int C = vc.C, Cp = vc.Cp;
+  unsigned long long* dir = vc.dir + bh * n;
+  unsigned long long* meta = vc.slots + bh * (size_t)(C + k);
+  unsigned long long* assign = meta + C;
+  const unsigned long long gen = ld_relaxed_gpu_u64(vc.stats + bh * 4);
+  const unsigned long long now = (gen + 1) << 32;
+  int* pchunk = reinterpret_cast<int*>(smem);                   // [k] chunk id at each position
+  int* pslot = pchunk + k;                                      // [k] hit slot, or -1
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem + ((2 * k * 4 + 7) & ~7));   // [Cp]
+  unsigned* val = reinterpret_cast<unsigned*>(key + Cp);        // [Cp] slot index
+  for (int p = tid; p < k; p += NT) {                           // 1. the whole selection (every rank has
+    int v;                                                      //    published or is about to)
+    const uint64_t t0 = globaltimer();
+    while ((v = ld_relaxed_gpu(slots_pub + p)) == 0) { __nanosleep(32); spin_guard(t0); }
+    const int j = v - 1;
+    pchunk[p] = j;
+    const unsigned long long e = ld_relaxed_gpu_u64(dir + j);
+    const unsigned tag = (unsigned)(e >> 32);
+    pslot[p] = (tag != 0u && tag <= (unsigned)gen) ? (int)(unsigned)e : -1;
+  }
+  for (int sl = tid; sl < Cp; sl += NT) {                       // 2. LRS keys of the slots
+    key[sl] = sl < C ? ld_relaxed_gpu_u64(meta + sl) : ~0ull;
+    val[sl] = (unsigned)sl;
+  }
+  __syncthreads();
+  for (int p = tid; p < k; p += NT)
+    if (pslot[p] >= 0) key[pslot[p]] = ~0ull;                   // hit this step: never a victim
+  __syncthreads();
+  for (int kk = 2; kk <= Cp; kk <<= 1) {                        // bitonic sort of (key, slot), ascending
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int i = tid; i < Cp; i += NT) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const bool up = (i & kk) == 0;
+          const unsigned long long a = key[i], b = key[ixj];
+          if ((a > b) == up) {
+            key[i] = b; key[ixj] = a;
+            const unsigned t = val[i]; val[i] = val[ixj]; val[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // 3 + 4. misses in position order take the smallest keys in order
+  const int per = (k + NT - 1) / NT;
+  const int pa = min(k, tid * per), pb = min(k, pa + per);
+  int nm = 0;
+  for (int p = pa; p < pb; ++p) nm += pslot[p] < 0;
+  int tot;
+  int r = block_exclusive_scan<NT>(nm, tk, &tot);
+  for (int p = pa; p < pb; ++p) {
+    const int j = pchunk[p];
+    if (pslot[p] >= 0) {                                        // hit: touched in this generation
+      st_relaxed_gpu_u64(meta + pslot[p], now | (unsigned long long)(j + 1));
+      continue;
+    }
+    const unsigned sl = val[r];
+    const unsigned long long old = key[r++];                    // the victim's state (0 = empty slot)
+    if (old != 0ull) st_relaxed_gpu_u64(dir + ((unsigned)old - 1u), 0ull);   // evicted chunk leaves the directory
+    st_relaxed_gpu_u64(dir + j, now | sl);
+    st_relaxed_gpu_u64(meta + sl, now | (unsigned long long)(j + 1));
+    st_relaxed_gpu_u64(assign + p, now | sl);                   // the unit holding this miss polls it
+  }
+}
+
 template <int G, bool ZSMEM>
 __global__ void __cluster_dims__(kSelCL, 1, 1) __launch_bounds__(kSelThreads, 2)
 k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ part, int tiles_per_head,
          float* __restrict__ zws, int32_t* __restrict__ sel,
-         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int force_fb) {
+         int32_t* __restrict__ selrest, int* __restrict__ flags, int32_t* __restrict__ sel_user, int force_fb,
+         VcArgs vc) {
   TRACE_INIT;
   constexpr int NT = kSelThreads, NW = NT / 32;
   extern __shared__ __align__(16) float zdyn[];
@@ -621,6 +715,11 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
     }
   }
   trace(1, 7);
+  // value cache (R26): rank 0 turns this step's selection into slot assignments
+  if (vc.dir != nullptr && crank == 0) {
+    __syncthreads();
+    vc_assign<NT>(vc, sel + bh * k, bh, n, k, reinterpret_cast<uint8_t*>(zdyn), tk);
+  }
 }
 
 // =============================================================================================
@@ -897,6 +996,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   int ntok;
   int vc_id = -1;                              // value cache: this thread's chunk and the call's generation
   unsigned long long vc_gen = 0;
+  bool vc_hit = false;                         // (a hit stays in its slot; a miss is written to the slot
+                                               //  the selector assigns, k_select's vc_assign)
   const int tx = tid & 15, ty = tid >> 4;      // exact-key tile ownership: tokens ty + 16 i (i < 4), dims tx*8..+8
   float acc[4][8];
   if (rebuild) {
@@ -945,9 +1046,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                              // the previous call's generation bump)
         vc_gen = ld_relaxed_gpu_u64(Ly.vc_stats + (size_t)bh * 4);
         const unsigned long long e = ld_relaxed_gpu_u64(Ly.vc_dir + (size_t)bh * D.n_c + id);
-        const unsigned tag = (unsigned)vc_gen;
-        if (tag != 0u && (unsigned)(e >> 32) == tag) {
-          vsrc = Ly.vc_values + (((size_t)bh * 2 + ((vc_gen - 1) & 1)) * D.k + (unsigned)e) * (kChunk * kHeadDim);
+        const unsigned tag = (unsigned)(e >> 32);         // inserting generation + 1; 0 = not cached
+        if (tag != 0u && tag <= (unsigned)vc_gen) {        // cached by an earlier step and still resident
+          vsrc = Ly.vc_values + ((size_t)bh * Ly.vc_cap + (unsigned)e) * (kChunk * kHeadDim);
+          vc_hit = true;
           atomicAdd(Ly.vc_stats + (size_t)bh * 4 + 1, 1ull);
         }
       }
@@ -1157,12 +1259,16 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   // as they arrive, so only the last chunk's 8 tokens remain once the host link delivers it.  The
   // result does not depend on the arrival order: per-chunk partial sums, combined in chunk order.
   const int nvb = kind == 0 ? nch : 1;                   // value barriers of this unit
-  auto vc_write_back = [&]() {                           // this step's selection becomes the cache (R26)
-    const int slot = ui * 8 + tid;                       // deterministic position in the selection
+  auto vc_write_back = [&]() {                           // a missed chunk enters the cache (R26)
+    if (vc_hit) return;
+    const int pos = ui * 8 + tid;                        // its position in the published selection
+    const unsigned long long* as = Ly.vc_slots + (size_t)bh * (Ly.vc_cap + D.k) + Ly.vc_cap + pos;
+    const uint64_t t0 = globaltimer();
+    unsigned long long a;
+    while ((unsigned)((a = ld_relaxed_gpu_u64(as)) >> 32) != (unsigned)(vc_gen + 1)) { __nanosleep(32); spin_guard(t0); }
     fence_proxy_async();
-    bulk_s2g(Ly.vc_values + (((size_t)bh * 2 + (vc_gen & 1)) * D.k + slot) * (kChunk * kHeadDim),
-             Vs + tid * kChunk * kHeadDim, kChunk * kHeadDim * 2);
-    Ly.vc_dir[(size_t)bh * D.n_c + vc_id] = ((vc_gen + 1) << 32) | (unsigned)slot;
+    bulk_s2g(Ly.vc_values + ((size_t)bh * Ly.vc_cap + (unsigned)a) * (kChunk * kHeadDim), Vs + tid * kChunk * kHeadDim,
+             kChunk * kHeadDim * 2);
   };
   if constexpr (G >= 8) {
     // ---- PV on the tensor cores: O[16][128] = P[16][64] . V[64][128], mma.sync m16n8k8 TF32 (values bf16:
@@ -1351,6 +1457,7 @@ static cudaError_t set_decode_attrs_g() {
   if ((e = cudaFuncGetAttributes(&fa, k_score<G>))) return e;
   if ((e = cudaFuncSetAttribute(k_score<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes))) return e;
   if ((e = cudaFuncSetAttribute(k_select<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelectSmemMax))) return e;
+  if ((e = cudaFuncSetAttribute(k_select<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelectSmemMax))) return e;
   if ((e = cudaFuncSetAttribute(k_sparse_attn<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)attn_smem_layout(256, G).bytes))) return e;
   return cudaSuccess;
@@ -1413,13 +1520,20 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
     const int force_fb = fb ? atoi(fb) : 0;               // before / after the definite chunks publish
     nvtxRangePushA("skv::select");
     const bool zsm = z_fits_smem(D, G);
-    const size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
+    size_t sel_smem = zsm ? (size_t)(((D.n_c + kSelCL - 1) / kSelCL + 3) & ~3) * 4 : 0;
+    VcArgs vc{Ly.vc_dir, Ly.vc_stats, Ly.vc_slots, Ly.vc_cap, 1};
+    if (Ly.vc_dir) {                                      // the value cache's slot assignment (R26)
+      while (vc.Cp < vc.C) vc.Cp <<= 1;
+      const size_t vb = vc_assign_smem_bytes(D.k, vc.Cp);
+      if (vb > kSelectSmemMax) return cudaErrorInvalidValue;
+      if (vb > sel_smem) sel_smem = vb;
+    }
     if (zsm) e = launch_pdl(!D.serial, k_select<G, true>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                             (const float*)ws.logits, (const float2*)ws.part, tph, ws.z,
-                            ws.sel, ws.selrest, ws.flags, sel_ids, force_fb);
+                            ws.sel, ws.selrest, ws.flags, sel_ids, force_fb, vc);
     else e = launch_pdl(!D.serial, k_select<G, false>, dim3(D.b * D.hk * kSelCL), dim3(kSelThreads), sel_smem, st, D,
                         (const float*)ws.logits, (const float2*)ws.part, tph, ws.z,
-                        ws.sel, ws.selrest, ws.flags, sel_ids, force_fb);
+                        ws.sel, ws.selrest, ws.flags, sel_ids, force_fb, vc);
     nvtxRangePop();
     if (e) return e;
     if (prof) { profile_mark(prof, kSelect, true, st); profile_mark(prof, kSparseAttn, false, st); }
@@ -1546,9 +1660,10 @@ cudaError_t launch_decode(const Dims& D, const Rope& R, const Layer& Ly, const u
     L.V_host = Ly.V_host + (size_t)r0 * hk * s * d;
     if (D.lr_A) { Ds.lr_A = D.lr_A + (size_t)r0 * D.wcap * D.r; Ds.lr_B = L.B; }
     if (Ly.vc_dir) {
-      L.vc_values = Ly.vc_values + (size_t)r0 * hk * 2 * D.k * kChunk * d;
+      L.vc_values = Ly.vc_values + (size_t)r0 * hk * Ly.vc_cap * kChunk * d;
       L.vc_dir = Ly.vc_dir + (size_t)r0 * hk * D.n_c;
       L.vc_stats = Ly.vc_stats + (size_t)r0 * hk * 4;
+      L.vc_slots = Ly.vc_slots + (size_t)r0 * hk * (Ly.vc_cap + D.k);
     }
     DecodeWs ws;
     decode_ws_bytes(Ds, &ws, ws_base + offs[i]);

@@ -45,10 +45,13 @@ struct Layer {
   uint16_t *K_out, *V_out, *K_win, *V_win;
   const uint16_t* V_host;
   uint16_t* A_gen;                    // optional low-rank generated keys [b][wcap][r] (NEXT-4)
-  // optional value-chunk cache (R26); all null = off
-  uint16_t* vc_values;                // [b][hk][2][k*c][d]
-  unsigned long long* vc_dir;         // [b][hk][n_c]  (tag << 32) | slot
+  // optional value-chunk cache (R26): least-recently-selected, capacity vc_cap slots; all null = off
+  uint16_t* vc_values;                // [b][hk][C][c][d]
+  unsigned long long* vc_dir;         // [b][hk][n_c]  (tag << 32) | slot; tag = inserting generation + 1
   unsigned long long* vc_stats;       // [b][hk][4]    {generation, step hits (scratch), last hits, total hits}
+  unsigned long long* vc_slots;       // [b][hk][C + k] per slot ((last generation + 1) << 32) | (chunk + 1);
+                                      //                then the step's miss -> slot assignments {slot, gen + 1}
+  int vc_cap;                         // C >= k
 };
 
 // workspace carving (256-B aligned regions)
@@ -77,6 +80,7 @@ constexpr int kUnitTok = 64;                      // tokens per attention unit (
 constexpr size_t kSelectSmemMax = 160 * 1024;     // per-CTA z slice + its logits kept in smem
 constexpr int kSelCL = 8;                         // select: CTAs per (request, KV head) cluster
 constexpr int kSelThreads = 512;
+constexpr int kMaxVcCapacity = 4096;              // value-cache slots per (request, KV head)
 constexpr int kSelCandLocal = 1024;               // threshold-bucket candidates of a cluster (all ranks)
 constexpr int kSelCandPush = 128;                 // threshold-bucket candidates per CTA (more: radix fallback)
 

@@ -110,8 +110,9 @@ def shard_state(state, p: Plan):
     t = dict(A=req(state.A), B=head(state.B), landmarks=head(state.landmarks), outlier_ids=head(state.outlier_ids),
              K_out=head(state.K_out), V_out=head(state.V_out), K_win=head(state.K_win), V_win=head(state.V_win),
              V_host=head(state.V_host), A_gen=req(state.A_gen), vc_values=head(state.vc_values),
-             vc_dir=head(state.vc_dir), vc_stats=head(state.vc_stats))
+             vc_dir=head(state.vc_dir), vc_stats=head(state.vc_stats), vc_slots=head(state.vc_slots),
+             vc_capacity=state.vc_capacity)
     for k, v in t.items():
-        if v is not None and not v.is_contiguous():
+        if isinstance(v, torch.Tensor) and not v.is_contiguous():
             raise ValueError(f"shard view of {k} is not contiguous")
     return LayerState.from_tensors(shape, state.A.device, **t)

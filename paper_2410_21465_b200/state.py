@@ -74,7 +74,7 @@ class LayerState:
     """One layer's tensors for the whole per-GPU batch."""
 
     def __init__(self, shape: Shape, device="cuda", V_host: torch.Tensor | None = None,
-                 value_cache: bool = False, lowrank_gen: bool = False):
+                 value_cache: bool = False, lowrank_gen: bool = False, vc_capacity: int = 0):
         self.shape = S = shape
         bd.ensure_init(device)                          # shadowkv_init for this device (once)
         b, hk, d = S.batch, S.n_kv_heads, S.head_dim
@@ -96,15 +96,19 @@ class LayerState:
             V_host = torch.empty(b, hk, S.ctx_len, d, dtype=bf, pin_memory=True)
         assert V_host.is_pinned() and V_host.shape == (b, hk, S.ctx_len, d)
         self.V_host = V_host
-        # optional GPU-resident value-chunk cache (skv_layer.vc_*, DESIGN R26): two slot buffers of
-        # k chunks per (request, KV head), the chunk directory and the hit counters
+        # optional GPU-resident value-chunk cache (skv_layer.vc_*, DESIGN R26): C = vc_capacity (0: k) value
+        # slots per (request, KV head), the chunk directory, the hit counters and the per-slot state
         # optional low-rank generated keys (skv_layer.A_gen, NEXT-4): one rank-r row per generated token
         self.A_gen = torch.zeros(b, S.window_cap, S.rank, dtype=bf, device=device) if lowrank_gen else None
-        self.vc_values = self.vc_dir = self.vc_stats = None
+        self.vc_values = self.vc_dir = self.vc_stats = self.vc_slots = None
+        self.vc_capacity = 0
         if value_cache:
-            self.vc_values = torch.empty(b, hk, 2, S.budget * S.chunk, d, dtype=bf, device=device)
+            C = vc_capacity or S.budget
+            self.vc_capacity = C
+            self.vc_values = torch.empty(b, hk, C, S.chunk, d, dtype=bf, device=device)
             self.vc_dir = torch.zeros(b, hk, S.n_c, dtype=torch.int64, device=device)
             self.vc_stats = torch.zeros(b, hk, 4, dtype=torch.int64, device=device)
+            self.vc_slots = torch.zeros(b, hk, C + S.budget, dtype=torch.int64, device=device)
 
     @classmethod
     def from_tensors(cls, shape: Shape, device, **tensors) -> "LayerState":
@@ -118,14 +122,15 @@ class LayerState:
             self.lens_host = torch.tensor(shape.ctx_lens, dtype=torch.int32)
             self.lens_dev = self.lens_host.to(device)
         for k in ("A", "B", "landmarks", "outlier_ids", "K_out", "V_out", "K_win", "V_win", "V_host", "A_gen",
-                  "vc_values", "vc_dir", "vc_stats"):
+                  "vc_values", "vc_dir", "vc_stats", "vc_slots"):
             setattr(self, k, tensors.get(k))
+        self.vc_capacity = int(tensors.get("vc_capacity", 0))
         return self
 
     def layer(self) -> bd.SkvLayer:
         return bd.layer_struct(self.A, self.B, self.landmarks, self.outlier_ids, self.K_out, self.V_out,
                                self.K_win, self.V_win, self.V_host, self.vc_values, self.vc_dir, self.vc_stats,
-                               self.A_gen)
+                               self.A_gen, self.vc_slots, self.vc_capacity)
 
     def cache_stats(self):
         """-> int64 [b][h_kv][4] {generation, -, hits in the last step, hits in total} (synchronises)."""

@@ -56,14 +56,15 @@ class Problem:
     """Seeded synthetic inputs for one layer (synth), the GPU state and the oracle state."""
 
     def __init__(self, cfg: synth.Config, seed: int, steps: int = 4, K_rope: bool = False, device="cuda",
-                 value_cache: bool = False, q_len: int = 1, lowrank_gen: bool = False):
+                 value_cache: bool = False, q_len: int = 1, lowrank_gen: bool = False, vc_capacity: int = 0):
         from paper_2410_21465_b200 import LayerState, RopeTable, Shape, alloc_workspace
         self.cfg, self.seed, self.steps = cfg, seed, steps
         self.inputs = synth.gen_layer(cfg, seed)
         self.inv, self.rot, self.il = synth.rope_table(cfg)
         self.q_len = q_len
         self.shape = Shape.from_config(cfg, steps=steps, q_len=q_len)
-        self.st = LayerState(self.shape, device=device, value_cache=value_cache, lowrank_gen=lowrank_gen)
+        self.st = LayerState(self.shape, device=device, value_cache=value_cache, lowrank_gen=lowrank_gen,
+                             vc_capacity=vc_capacity)
         self.st.A.copy_(self.inputs["A"]); self.st.B.copy_(self.inputs["B"])
         self.st.V_host.copy_(self.inputs["V"])
         self.rope = RopeTable(self.inv, self.rot, self.il, device=device)

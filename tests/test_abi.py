@@ -27,7 +27,7 @@ def test_header_declares_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert bd.shadowkv_abi_version() == 6
+    assert bd.shadowkv_abi_version() == 7
 
 
 def _dims(**kw):
@@ -89,10 +89,12 @@ def test_decode_argument_errors_before_any_cuda_call(lib):
     st = lib.shadowkv_build_cache(ctypes.byref(d), ctypes.byref(rope), ctypes.byref(bad), None, 256, None)
     assert st == bd.SKV_EINVAL
     assert lib.shadowkv_decode_step(None, None, None, 0, 0, 0, 0, 0, None, None, 0, None) == bd.SKV_EINVAL
-    partial = bd.SkvLayer(*([16] * 9 + [16, None, 16]))     # value cache: all three pointers or none
+    partial = bd.SkvLayer(*([16] * 9 + [16, None, 16]))     # value cache: all four pointers or none
     assert call(layer=partial) == bd.SKV_EINVAL and "vc_" in lib.shadowkv_last_error().decode()
-    misal = bd.SkvLayer(*([16] * 9 + [16, 24, 16]))
+    misal = bd.SkvLayer(*([16] * 9 + [16, 24, 16, None, 16]))
     assert call(layer=misal) == bd.SKV_EINVAL and "aligned" in lib.shadowkv_last_error().decode()
+    small = bd.SkvLayer(*([16] * 9 + [16, 16, 16, None, 16, 1]))   # capacity below the budget
+    assert call(layer=small) == bd.SKV_EINVAL and "vc_capacity" in lib.shadowkv_last_error().decode()
     gen_misal = bd.SkvLayer(*([16] * 9 + [None, None, None, 24]))  # low-rank generated keys (NEXT-4)
     assert call(layer=gen_misal) == bd.SKV_EINVAL and "A_gen" in lib.shadowkv_last_error().decode()
 

@@ -3,8 +3,8 @@
 * Outputs and selections with the cache are bit-identical to the same GPU path without it (cached
   values are bit copies), and match the fp64 oracle within the decode tolerances (R1, R23).
 * The per-step hit counts the kernels report equal, bit-exact, the oracle's least-recently-selected
-  cache (capacity k, oracle.ValueChunkCache) replayed over the GPU's own selection trace, and the
-  oracle's own trace wherever the two selections agree.
+  cache (capacity C = k and C = 3k, oracle.ValueChunkCache) replayed over the GPU's own selection trace,
+  and the oracle's own trace wherever the two selections agree.
 * Queries drift (synth.gen_q_drift, R27) so consecutive selections overlap.
 """
 import numpy as np
@@ -45,14 +45,16 @@ def _twin_without_cache(P):
     return ref
 
 
+@pytest.mark.parametrize("cap", [1, 3])
 @pytest.mark.parametrize("name", list(CASES))
-def test_value_cache_parity_and_hits(name):
+def test_value_cache_parity_and_hits(name, cap):
     cfg = CASES[name]
     steps = 8
-    P = Problem(cfg, seed=5, steps=steps, value_cache=True)
+    C = cap * cfg.budget
+    P = Problem(cfg, seed=5, steps=steps, value_cache=True, vc_capacity=C)
     ost = P.oracle_build()
     P.load_state_from_oracle(ost)
-    P.st.vc_dir.zero_(); P.st.vc_stats.zero_()
+    P.st.vc_dir.zero_(); P.st.vc_stats.zero_(); P.st.vc_slots.zero_()
     ref = _twin_without_cache(P)
     b, hk, k = cfg.batch, cfg.n_kv_heads, cfg.budget
     gtrace = [[[] for _ in range(hk)] for _ in range(b)]
@@ -72,11 +74,11 @@ def test_value_cache_parity_and_hits(name):
             for h in range(hk):
                 gtrace[bi][h].append(gsel[bi, h])
                 otrace[bi][h].append(osel[bi, h])
-                want = O.replay_hits(gtrace[bi][h], k)
+                want = O.replay_hits(gtrace[bi][h], C)
                 assert stats[bi, h, 2] == want[-1], f"step {t} b={bi} h={h}: gpu hits {stats[bi, h, 2]} != {want[-1]}"
                 assert stats[bi, h, 3] == want.sum()
                 if all(np.array_equal(x, y) for x, y in zip(gtrace[bi][h], otrace[bi][h])):
-                    assert stats[bi, h, 2] == O.replay_hits(otrace[bi][h], k)[-1]
+                    assert stats[bi, h, 2] == O.replay_hits(otrace[bi][h], C)[-1]
         total = int(stats[..., 3].sum())
     assert total > 0, "drifting queries produced no cache hits"
     P.gpu_build()                                                  # a new prefill resets the cache
@@ -92,7 +94,7 @@ def test_value_cache_graph_replay():
     ost = P.oracle_build()
     P.load_state_from_oracle(ost)
     win0 = (P.st.K_win.clone(), P.st.V_win.clone())
-    P.st.vc_dir.zero_(); P.st.vc_stats.zero_()
+    P.st.vc_dir.zero_(); P.st.vc_stats.zero_(); P.st.vc_slots.zero_()
     inputs = _drift_inputs(cfg, 9, steps, 0.97)
     ref_out, ref_hits = [], []
     for t, si in enumerate(inputs):
@@ -100,7 +102,7 @@ def test_value_cache_graph_replay():
         ref_out.append(gout)
         ref_hits.append(P.st.cache_stats().numpy()[..., 2].copy())
     P.st.K_win.copy_(win0[0]); P.st.V_win.copy_(win0[1])
-    P.st.vc_dir.zero_(); P.st.vc_stats.zero_()
+    P.st.vc_dir.zero_(); P.st.vc_stats.zero_(); P.st.vc_slots.zero_()
     c = cfg
     q_b = inputs[0]["q"].cuda().clone(); k_b = inputs[0]["k_new"].cuda().clone(); v_b = inputs[0]["v_new"].cuda().clone()
     out_b = torch.empty(c.batch, c.n_q_heads, c.head_dim, dtype=torch.bfloat16, device="cuda")
@@ -112,7 +114,7 @@ def test_value_cache_graph_replay():
             P.st.decode_dev(P.rope.struct, q_b, k_b, v_b, step_dev, steps - 1, out_b, P.ws, stream=side)
             step_dev.add_(1)
         torch.cuda.synchronize()
-        P.st.vc_dir.zero_(); P.st.vc_stats.zero_(); step_dev.fill_(0)   # capture does not execute; be explicit
+        P.st.vc_dir.zero_(); P.st.vc_stats.zero_(); P.st.vc_slots.zero_(); step_dev.fill_(0)   # capture does not execute; be explicit
         torch.cuda.synchronize()
         for t, si in enumerate(inputs):
             q_b.copy_(si["q"]); k_b.copy_(si["k_new"]); v_b.copy_(si["v_new"])

@@ -15,9 +15,11 @@ echo "bench rc=$?"
 python - <<EOF
 import json
 d = json.loads(open("gpurun_out/${TAG}_bench.json").read().strip().splitlines()[-1])
-print("value", round(d["value"], 1), "ms", round(d["ms_per_step"], 4), "frac", round(d["roofline"]["frac"], 3),
-      "vc", round(d.get("value_cache", {}).get("value", 0), 1), "alpha", round(d.get("value_cache", {}).get("alpha", 0), 3),
-      "vc_frac", round(d.get("value_cache", {}).get("step_frac_of_host_roofline", 0), 3))
+print("value", round(d["value"], 1), "ms", round(d["ms_per_step"], 4), "frac", round(d["roofline"]["frac"], 3))
+vc = d.get("value_cache") or []
+for leg in (vc if isinstance(vc, list) else [vc]):
+    print("  vc C/k", leg.get("capacity_over_k"), "value", round(leg.get("value", 0), 1), "alpha", round(leg.get("alpha", 0), 3),
+          "frac", round(leg.get("step_frac_of_host_roofline", 0), 3), leg.get("error", ""))
 EOF
 timeout 300 python tools/trace_run.py --slots 6 > gpurun_out/${TAG}_trace_c2.txt 2>&1
 head -9 gpurun_out/${TAG}_trace_c2.txt
