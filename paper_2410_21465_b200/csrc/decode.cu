@@ -1575,6 +1575,7 @@ static cudaError_t launch_decode_g(const Dims& D, const Rope& R, const Layer& Ly
   if (prof) profile_mark(prof, kCombine, true, st);
   *launches += 4;
 
+
   return cudaGetLastError();
 }
 

@@ -62,6 +62,36 @@ __device__ __forceinline__ void trace_tc_any(uint64_t* t, int ev) {   // caller 
   if (t != nullptr) t[(size_t)blockIdx.x * 16 + ev] = globaltimer();
 }
 
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+// Reduce-scatter of G values per lane over the warp (max or sum): rounds xor 16, 8, ... halve the payload
+// while it has more than one value, then finish with single-value rounds.  Lane l returns the reduction of
+// row (l >> (5 - log2 G)) over all 32 lanes.
+template <int G, bool kMax>
+__device__ __forceinline__ float rs_reduce(float (&v)[G], int lane) {
+  int n = G;
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    if (n > 1) {
+      const int half = n >> 1;
+      const bool up = (lane & m) != 0;
+#pragma unroll
+      for (int i = 0; i < G / 2; ++i) {
+        if (i < half) {
+          const float send = up ? v[i] : v[i + half];
+          const float keep = up ? v[i + half] : v[i];
+          const float got = __shfl_xor_sync(0xffffffffu, send, m);
+          v[i] = kMax ? fmaxf(keep, got) : keep + got;
+        }
+      }
+      n = half;
+    } else {
+      const float got = __shfl_xor_sync(0xffffffffu, v[0], m);
+      v[0] = kMax ? fmaxf(v[0], got) : v[0] + got;
+    }
+  }
+  return v[0];
+}
 }  // namespace
 
 cudaError_t set_trace_buffer_tc(void* p) { return cudaMemcpyToSymbol(g_trace_tc, &p, sizeof(void*)); }
@@ -240,12 +270,22 @@ k_score_tc(const __grid_constant__ CUtensorMap tmap, Dims D, const int32_t* __re
 #pragma unroll
       for (int hq = 0; hq < G; ++hq) xs[hq] = out ? -INFINITY : v[hq] * scale;
       if (j < D.n_c) store_row<G>(lrow + (size_t)j * G, xs);   // landmark-major logits [n_c][G]
+      // the warp's softmax partial per query row over its 32 landmarks: a reduce-scatter of the G row
+      // values (the lane ends with row r_lane's max), an all-gather of the G maxima, then a reduce-scatter
+      // of the exps: 3G + 5 - log2 G shuffles instead of 10G
+      {
+        float x2[G], e[G];
 #pragma unroll
-      for (int hq = 0; hq < G; ++hq) {
-        const float x2 = out ? kFloor : xs[hq] * kLog2e;
-        const float m2 = warp_max(x2);
-        const float sm = warp_sum(out ? 0.f : exp2f(x2 - m2));
-        if (lane == 0) wpart[grp][par][quad][hq] = make_float2(m2, sm);
+        for (int hq = 0; hq < G; ++hq) { x2[hq] = out ? kFloor : xs[hq] * kLog2e; e[hq] = x2[hq]; }
+        const float mr = rs_reduce<G, true>(e, lane);          // max of row r_lane
+        constexpr int kSh = 5 - ilog2(G);                       // row r lives in lanes (r << kSh) + ...
+#pragma unroll
+        for (int hq = 0; hq < G; ++hq) {
+          const float m = __shfl_sync(0xffffffffu, mr, hq << kSh);
+          e[hq] = out ? 0.f : exp2f(x2[hq] - m);
+        }
+        const float sr = rs_reduce<G, false>(e, lane);         // sum of row r_lane
+        if ((lane & ((1 << kSh) - 1)) == 0) wpart[grp][par][quad][lane >> kSh] = make_float2(mr, sr);
       }
       asm volatile("bar.sync %0, 128;" :: "r"(grp + 1) : "memory");   // the group's 4 warps
       if (quad == 0 && lane < G) {                        // fixed-order merge of the 4 warps (log2 domain)
