@@ -290,14 +290,14 @@ __host__ __device__ inline size_t vc_assign_smem_bytes(int k, int Cp) {
   return (size_t)2 * k * 4 + 8 + (size_t)Cp * 12;
 }
 template <int NT>
-__device__ __noinline__ void vc_assign(const VcArgs vc, const int32_t* slots_pub, size_t bh, int n, int k,
+__device__ __noinline__ void vc_assign(const VcArgs vc, unsigned long long gen, const int32_t* slots_pub, size_t bh,
+                                       int n, int k,
                                        uint8_t* smem, TopKSmem<NT>& tk) {
   const int tid = threadIdx.x;
   const int C = vc.C, Cp = vc.Cp;
   unsigned long long* dir = vc.dir + bh * n;
   unsigned long long* meta = vc.slots + bh * (size_t)(C + k);
   unsigned long long* assign = meta + C;
-  const unsigned long long gen = ld_relaxed_gpu_u64(vc.stats + bh * 4);
   const unsigned long long now = (gen + 1) << 32;
   int* pchunk = reinterpret_cast<int*>(smem);                   // [k] chunk id at each position
   int* pslot = pchunk + k;                                      // [k] hit slot, or -1
@@ -420,6 +420,9 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   pdl_wait();
   trace(1, 1);
   int* fl = flags + bh * 4;
+  // the value cache's generation of this step, read before any slot is published: the merge closes it
+  // once every unit of the head is done, which can precede vc_assign when all of them hit
+  const unsigned long long vc_gen = (vc.dir != nullptr && crank == 0) ? ld_relaxed_gpu_u64(vc.stats + bh * 4) : 0ull;
   // score (incl. a7 window append) complete.  A relaxed store: the score grid's writes reached L2 when it
   // completed (our griddepcontrol.wait), and the readers (outlier / window units) bulk-copy from L2; a
   // release here is a membar on the critical path of the barrier below
@@ -718,7 +721,7 @@ k_select(Dims D, const float* __restrict__ logits, const float2* __restrict__ pa
   // value cache (R26): rank 0 turns this step's selection into slot assignments
   if (vc.dir != nullptr && crank == 0) {
     __syncthreads();
-    vc_assign<NT>(vc, sel + bh * k, bh, n, k, reinterpret_cast<uint8_t*>(zdyn), tk);
+    vc_assign<NT>(vc, vc_gen, sel + bh * k, bh, n, k, reinterpret_cast<uint8_t*>(zdyn), tk);
   }
 }
 
