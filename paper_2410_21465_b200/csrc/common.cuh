@@ -82,6 +82,14 @@ namespace skv {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
+// Bounded polling: a flag that never arrives (a bug, or a grid that cannot become resident) aborts the
+// kernel with an error after ~2 s instead of hanging the device.  Call with the spin's start time.
+__device__ __forceinline__ void spin_guard(uint64_t t0) {
+  if (globaltimer() - t0 > 2000000000ull) __trap();
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
 }
@@ -94,10 +102,23 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+// Every mbarrier wait is bounded like the flag polls (spin_guard): a phase that never completes (a lost
+// TMA / tcgen05 completion, a bug) traps after ~2 s -- a sticky launch error the caller sees -- instead of
+// leaving the device hung.  The first try_wait (which itself suspends for a while) is the common exit.
+// (the bounded loop is out of line: inlined, its timer registers raise the register pressure of the
+// attention kernel)
+static __device__ __noinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try_wait(bar, parity)) spin_guard(t0);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
-               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-               " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+  if (!mbar_try_wait(bar, parity)) mbar_wait_bounded(bar, parity);
 }
 // non-blocking: has the phase with this parity completed?
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -248,14 +269,6 @@ __device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsign
 }
 __device__ __forceinline__ void st_relaxed_gpu(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
-}
-// Bounded polling: a flag that never arrives (a bug, or a grid that cannot become resident) aborts the
-// kernel with an error after ~2 s instead of hanging the device.  Call with the spin's start time.
-__device__ __forceinline__ void spin_guard(uint64_t t0) {
-  if (globaltimer() - t0 > 2000000000ull) __trap();
 }
 // spin (with backoff) until flag[0] != 0, then return flag[1] (read with acquire semantics by one
 // thread and broadcast through shared memory, so no thread can see a stale L1 copy)

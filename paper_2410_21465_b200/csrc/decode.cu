@@ -1102,7 +1102,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       int* ids = reinterpret_cast<int*>(As);
       for (int i = tid; i < D.k; i += 256) {
         int v;
-        while ((v = ld_relaxed_gpu(slots + i)) == 0) __nanosleep(32);
+        const uint64_t t0 = globaltimer();
+        while ((v = ld_relaxed_gpu(slots + i)) == 0) { __nanosleep(32); spin_guard(t0); }
         ids[i] = v - 1;
       }
       __syncthreads();
@@ -1304,7 +1305,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       if (kind == 0) {
         float2 pc[8];                                    // per-chunk partial sums
         unsigned pending = (1u << nvb) - 1u;
+        const uint64_t t0 = globaltimer();
         while (pending) {
+          spin_guard(t0);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             if (((pending >> c) & 1u) && mbar_test(&barVc[c], 0)) {
